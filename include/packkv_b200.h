@@ -1,0 +1,166 @@
+/*
+ * packkv_b200.h — C ABI of the B200-native PackKV hot path (libpackkv_b200.so).
+ *
+ * The reference (arXiv 2512.24449, /root/reference) ships a pure-Python API
+ * and no FFI: SPEC.md specifies the functions below as Python operations.
+ * Each entry point here replaces one of them (cited per function); the
+ * Python package paper_2512_24449_b200 binds them with ctypes exactly as a
+ * maintainer would bind them from packkv.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer owned by the caller (the library never
+ *     allocates or frees device memory; torch allocates arenas, tables,
+ *     scratch and outputs);
+ *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*);
+ *   - every call returns PKV_OK or a PKV_E_* status; pkv_last_error() gives a
+ *     thread-local message.  Data-dependent errors that only the device can
+ *     see (non-finite input, width overflow, malformed block) are OR-ed into
+ *     the caller's int32 `err` flag word as PKV_FLAG_* bits, to be checked by
+ *     the caller after a stream sync (the Python layer maps them onto
+ *     packkv.errors classes: NonFiniteValueError, WidthOverflowError,
+ *     MalformedBlockError — errors.py:20,28,32).
+ *   - fp16 tensors are passed as uint16_t* (raw IEEE binary16 bit patterns).
+ */
+#ifndef PACKKV_B200_H
+#define PACKKV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PKV_ABI_VERSION 1
+
+enum {
+  PKV_OK = 0,
+  PKV_E_SHAPE = 1,      /* ShapeMismatchError (errors.py:24)          */
+  PKV_E_NONFINITE = 2,  /* NonFiniteValueError (errors.py:20)         */
+  PKV_E_WIDTH = 3,      /* WidthOverflowError (errors.py:28)          */
+  PKV_E_MALFORMED = 4,  /* MalformedBlockError (errors.py:32)         */
+  PKV_E_INDEX = 5,      /* IndexError         */
+  PKV_E_ARG = 6,        /* ValueError: unsupported parameter          */
+  PKV_E_CUDA = 7,       /* CUDA launch / runtime failure              */
+  PKV_E_CAPACITY = 8    /* arena too small for the requested append   */
+};
+
+#define PKV_FLAG_NONFINITE 1
+#define PKV_FLAG_WIDTH 2
+#define PKV_FLAG_MALFORMED 4
+#define PKV_FLAG_CAPACITY 8
+
+#define PKV_KIND_K 0
+#define PKV_KIND_V 1
+#define PKV_LAYOUT_K_INTERLEAVED 0
+#define PKV_LAYOUT_V_CONTIGUOUS 1
+
+#define PKV_REPACK_NONE 0
+#define PKV_REPACK_GREEDY 1
+#define PKV_REPACK_V_MEDIAN 2
+
+/*
+ * One layer of a batched compressed store (SPEC.md:357-362 CompressedStore,
+ * one independent sub-store per layer).  `batch` sequences ×
+ * `heads` KV heads = units; unit u = b*heads + h.  Blocks are `block`(=64)
+ * tokens × head_dim channels, encoded per SPEC.md:330 and placed in `arena`
+ * at 16-byte-aligned offsets (zero padding between blocks).
+ */
+typedef struct pkv_layer {
+  int32_t batch;        /* sequences B                                  */
+  int32_t heads;        /* KV heads per sequence H                      */
+  int32_t head_dim;     /* D (32, 64, 128 or 256)                       */
+  int32_t block;        /* tokens per block (64)                        */
+  int32_t pack_size;    /* k in {2,4,8,16,32}                           */
+  int32_t buffer;       /* staging capacity in tokens (128)             */
+  int32_t max_blocks;   /* block-table capacity per unit                */
+  int32_t reserved;
+  uint8_t* arena;       /* append-only byte arena                       */
+  int64_t arena_capacity;
+  int64_t* tail;        /* [1] bytes used (16-aligned)                  */
+  int64_t* blk_off;     /* [2][B*H][max_blocks] byte offset per block   */
+  int32_t* blk_len;     /* [2][B*H][max_blocks] byte length per block   */
+  uint8_t* perm;        /* [B][max_blocks][block] repack permutation    */
+  int32_t* nblk;        /* [B] blocks per sequence                      */
+  int32_t* nres;        /* [B] staged (uncompressed residue) tokens     */
+  uint16_t* stage;      /* [2][B*H][buffer][D] fp16 staging ring        */
+  int32_t* err;         /* [1] PKV_FLAG_* bits                          */
+} pkv_layer_t;
+
+const char* pkv_last_error(void);
+int pkv_version(void);
+
+/* --- quantizer -------------------------------------- */
+/* quantize_token_wise over n independent [rows, cols] fp16 tensors.
+ * q: [n][rows][cols] uint16 codes; params: [n][rows][2] f32 (scale, zp). */
+int pkv_quantize(const uint16_t* x, int32_t n, int32_t rows, int32_t cols, float rel,
+                 uint16_t* q, float* params, int32_t* err, void* stream);
+/* HalfTensor ingestion check: ORs PKV_FLAG_NONFINITE into *err
+ * if any of the n fp16 values is NaN or infinite.                          */
+int pkv_check_finite(const uint16_t* x, int64_t n, int32_t* err, void* stream);
+/* dequantize: out = q*scale + zp in f32 (mul then add). */
+int pkv_dequantize(const uint16_t* q, const float* params, int32_t n, int32_t rows,
+                   int32_t cols, float* out, void* stream);
+
+/* --- bitpack codec over independent blocks ------------ */
+/* encode_block, pass 1: exact encoded byte length of each block.
+ * q/params as produced by pkv_quantize; params may be NULL (zeros).        */
+int pkv_encode_sizes(const uint16_t* q, int32_t n, int32_t rows, int32_t cols,
+                     int32_t pack_size, int32_t layout, int64_t* sizes, int32_t* err,
+                     void* stream);
+/* encode_block, pass 2: write block i at out + offsets[i] (any alignment). */
+int pkv_encode(const uint16_t* q, const float* params, int32_t n, int32_t rows, int32_t cols,
+               int32_t pack_size, int32_t layout, int32_t kind, const int64_t* offsets,
+               uint8_t* out, int32_t* err, void* stream);
+/* decode_block: validates each header and length
+ * (MalformedBlockError) and writes codes [n][rows][cols] + params f32
+ * widened from the f16 wire fields.                                        */
+int pkv_decode(const uint8_t* buf, const int64_t* offsets, const int64_t* lens, int32_t n,
+               int32_t rows, int32_t cols, uint16_t* q, float* params, int32_t* err,
+               void* stream);
+/* decode_pack_at: k values of physical pack `pack_index`
+ * of each block (index-range errors are raised host-side).                 */
+int pkv_decode_pack_at(const uint8_t* buf, const int64_t* offsets, int32_t n, int32_t pack_index,
+                       uint16_t* out, void* stream);
+
+/* --- store: append_token / compress_batch ------------- */
+/* Scratch bytes needed by pkv_compress_tokens for `nsets` block-sets.      */
+int64_t pkv_compress_scratch_bytes(const pkv_layer_t* L, int32_t nsets);
+/* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:
+ * [B][ntok][H][D] fp16.  `staged` = tokens already staged per sequence
+ * (host mirror of nres, < block); `nblocks_before` = blocks per sequence
+ * before the call (host mirror of nblk).  Every full block of 64 is quantized
+ * (rel_k / rel_v), repacked (`repack`, one permutation per (sequence,
+ * block-set) shared by K, V and all heads), encoded (K layout
+ * k_interleaved, V layout v_contiguous) and appended in arena order
+ * (block-set, sequence, kind K then V, head); the remainder is staged.     */
+int pkv_compress_tokens(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new,
+                        int32_t ntok, int32_t staged, int32_t nblocks_before, float rel_k,
+                        float rel_v, int32_t repack, void* scratch, int64_t scratch_bytes,
+                        void* stream);
+
+/* --- fused decompress + GEMV --------------------------- */
+/* scores[b][hq][t] = sum_c deq(K[b, hq/G][t][c]) * q[b][hq][c], t over the
+ * blocks in directory (permuted-row) order then the residue; G = q_heads /
+ * heads query heads share each decoded tile (GQA).  q: [B][q_heads][D] f32;
+ * scores: [B][q_heads][score_stride] f32.  `nblocks` = max blocks per
+ * sequence (host mirror of nblk; sizes the grid).                          */
+int pkv_fused_k_scores(const pkv_layer_t* L, int32_t nblocks, const float* q, int32_t q_heads,
+                       float* scores, int64_t score_stride, void* stream);
+/* Scratch bytes for pkv_fused_v_output (split-L partials).                 */
+int64_t pkv_fused_v_scratch_bytes(const pkv_layer_t* L, int32_t nblocks, int32_t q_heads);
+/* out[b][hq][c] = sum_t w[b][hq][t] * deq(V[b, hq/G][t][c]), deterministic
+ * fixed-order split-L reduction.  w: [B][q_heads][w_stride]. */
+int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const float* w, int32_t q_heads,
+                       int64_t w_stride, float* out, void* scratch, int64_t scratch_bytes,
+                       void* stream);
+
+/* --- parity / debug ------------------------------------------------------ */
+/* Decodes every block of one kind into codes [B*H][max_blocks][block][D]
+ * (block-row order) and params [B*H][max_blocks][block][2] f32.            */
+int pkv_decode_store(const pkv_layer_t* L, int32_t kind, uint16_t* codes, float* params,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PACKKV_B200_H */

@@ -1,0 +1,347 @@
+"""Appendable compressed KV store, device resident.
+
+A ``CompressedStore`` holds ``layers`` independent sub-stores,
+each for a batch of ``batch`` sequences × ``heads`` KV heads.  Per layer the
+HBM layout is:
+
+  arena     uint8 [capacity]            PackedBlocks at 16-byte aligned offsets
+  blk_off   int64 [2, B*H, max_blocks]  block directory: byte offset per block
+  blk_len   int32 [2, B*H, max_blocks]  exact block length (SPEC.md:330 bytes)
+  perm      uint8 [B, max_blocks, 64]   shared K/V repack permutation per block-set
+  nblk/nres int32 [B]                   blocks / staged residue tokens per sequence
+  stage     fp16  [2, B*H, buffer, D]   uncompressed staging ring
+
+``append_token`` / ``compress_batch`` enqueue the device
+compressor (csrc/store.cu) on the current stream; the host keeps mirrors of
+the token counts so no device round trip is needed to decide flushes, and an
+upper bound of the arena tail so capacity is only synchronised when it may run
+out.  Sequences advance in lockstep (every call appends the same tokens count
+to every sequence of the batch).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import errors as E
+from .bitpack_codec import header_bytes
+
+KIND_K, KIND_V = 0, 1
+REPACK_STRATEGIES = ("none", "greedy", "v_median")
+
+
+def _round16(x: int) -> int:
+    return (x + 15) & ~15
+
+
+def max_block_bytes(rows: int, cols: int, k: int) -> int:
+    return header_bytes(rows, cols, k) + (rows // k) * cols * ((k * 15 + 7) // 8)
+
+
+@dataclass
+class BlockDirectoryEntry:
+    """SPEC.md:351-356 (plus the sequence index of a batched store)."""
+    kind: int
+    layer: int
+    head: int
+    token_start: int
+    token_end: int
+    byte_offset: int
+    byte_len: int
+    permutation: np.ndarray
+    seq: int = 0
+
+
+@dataclass
+class ResidueHandle:
+    """Terminal handle of iterate_blocks: the staged, uncompressed tokens."""
+    layer: int
+    token_start: int
+    tokens: int
+    seq: int = 0
+
+
+class LayerStore:
+    """One layer's device-resident sub-store (see module docstring)."""
+
+    def __init__(self, owner: "CompressedStore", layer: int, init_blocks: int):
+        self.owner = owner
+        self.layer = layer
+        o = owner
+        dev = o.device
+        U = o.batch * o.heads
+        self.max_blocks = max(1, init_blocks)
+        self.blk_max = _round16(max_block_bytes(o.block, o.head_dim, o.pack_size))
+        cap = self._expected_bytes(self.max_blocks)
+        self.arena = torch.zeros(cap + 16, dtype=torch.uint8, device=dev)
+        self.tail = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.blk_off = torch.full((2, U, self.max_blocks), -1, dtype=torch.int64, device=dev)
+        self.blk_len = torch.zeros((2, U, self.max_blocks), dtype=torch.int32, device=dev)
+        self.perm = torch.zeros((o.batch, self.max_blocks, o.block), dtype=torch.uint8, device=dev)
+        self.nblk = torch.zeros(o.batch, dtype=torch.int32, device=dev)
+        self.nres = torch.zeros(o.batch, dtype=torch.int32, device=dev)
+        self.stage = torch.zeros((2, U, o.buffer, o.head_dim), dtype=torch.float16, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.scratch = torch.empty(0, dtype=torch.uint8, device=dev)
+        self.v_scratch = torch.empty(0, dtype=torch.uint8, device=dev)
+        # host mirrors
+        self.nblk_h = 0
+        self.nres_h = 0
+        self.tail_ub = 0
+        self._struct = None
+
+    # -- geometry ---------------------------------------------------------------
+    def _expected_bytes(self, blocks: int) -> int:
+        o = self.owner
+        # typical compressed block ~ raw/4; start there and grow geometrically
+        per = _round16(header_bytes(o.block, o.head_dim, o.pack_size) + o.block * o.head_dim // 2)
+        return max(1 << 16, blocks * 2 * o.batch * o.heads * per)
+
+    @property
+    def capacity(self) -> int:
+        return int(self.arena.numel()) - 16
+
+    def struct(self) -> N.Layer:
+        if self._struct is None:
+            o = self.owner
+            s = N.Layer()
+            s.batch, s.heads, s.head_dim, s.block = o.batch, o.heads, o.head_dim, o.block
+            s.pack_size, s.buffer, s.max_blocks, s.reserved = o.pack_size, o.buffer, self.max_blocks, 0
+            s.arena, s.arena_capacity = N.ptr(self.arena), self.capacity
+            s.tail, s.blk_off, s.blk_len = N.ptr(self.tail), N.ptr(self.blk_off), N.ptr(self.blk_len)
+            s.perm, s.nblk, s.nres = N.ptr(self.perm), N.ptr(self.nblk), N.ptr(self.nres)
+            s.stage, s.err = N.ptr(self.stage), N.ptr(self.err)
+            self._struct = s
+        return self._struct
+
+    @property
+    def tokens(self) -> int:
+        return self.nblk_h * self.owner.block + self.nres_h
+
+    # -- growth -----------------------------------------------------------------
+    def _grow_tables(self, need_blocks: int):
+        o = self.owner
+        new = max(need_blocks, 2 * self.max_blocks)
+        U = o.batch * o.heads
+        off = torch.full((2, U, new), -1, dtype=torch.int64, device=o.device)
+        ln = torch.zeros((2, U, new), dtype=torch.int32, device=o.device)
+        pm = torch.zeros((o.batch, new, o.block), dtype=torch.uint8, device=o.device)
+        off[:, :, :self.max_blocks] = self.blk_off
+        ln[:, :, :self.max_blocks] = self.blk_len
+        pm[:, :self.max_blocks] = self.perm
+        self.blk_off, self.blk_len, self.perm, self.max_blocks = off, ln, pm, new
+        self._struct = None
+
+    def _ensure(self, nsets: int):
+        o = self.owner
+        if self.nblk_h + nsets > self.max_blocks:
+            self._grow_tables(self.nblk_h + nsets)
+        need = nsets * 2 * o.batch * o.heads * self.blk_max
+        if self.tail_ub + need > self.capacity:
+            self.tail_ub = int(self.tail.item())         # synchronise only when it may not fit
+            if self.tail_ub + need > self.capacity:
+                newcap = max(2 * self.capacity, self.tail_ub + need + self._expected_bytes(nsets))
+                arena = torch.zeros(newcap + 16, dtype=torch.uint8, device=o.device)
+                arena[:self.tail_ub] = self.arena[:self.tail_ub]
+                self.arena = arena
+                self._struct = None
+
+    # -- append -----------------------------------------------------------------
+    def compress(self, k_new: torch.Tensor, v_new: torch.Tensor, check: bool):
+        """k_new/v_new: fp16 [B, T, H, D] on the device, contiguous."""
+        o = self.owner
+        T = int(k_new.shape[1])
+        lib = N.lib()
+        strm = N.stream()
+        if check and T:
+            for x in (k_new, v_new):
+                N.check(lib.pkv_check_finite(N.ptr(x), x.numel(), N.ptr(self.err), strm), "append")
+            N.raise_flags(int(self.err.item()), "append")
+        total = self.nres_h + T
+        nsets = total // o.block
+        if total - nsets * o.block > o.buffer:
+            raise N.CapacityError("staging overflow")
+        if nsets:
+            self._ensure(nsets)
+        L = self.struct()
+        if nsets:
+            per_set = int(lib.pkv_compress_scratch_bytes(ctypes_ref(L), 1))
+            chunk = max(1, min(nsets, (256 << 20) // per_set))
+            need = per_set * chunk
+            if self.scratch.numel() < need:
+                self.scratch = torch.empty(need, dtype=torch.uint8, device=o.device)
+        N.check(lib.pkv_compress_tokens(ctypes_ref(L), N.ptr(k_new), N.ptr(v_new), T, self.nres_h, self.nblk_h,
+                                        float(o.rel_scale_k), float(o.rel_scale_v), N.REPACK[o.repack],
+                                        N.ptr(self.scratch), int(self.scratch.numel()), strm), "compress")
+        self.nblk_h += nsets
+        self.nres_h = total - nsets * o.block
+        self.tail_ub += nsets * 2 * o.batch * o.heads * self.blk_max
+        if check:
+            N.raise_flags(int(self.err.item()), "compress")
+
+    # -- introspection (synchronising; parity / debug) ----------------------------
+    def tables(self):
+        o = self.owner
+        U = o.batch * o.heads
+        nb = self.nblk_h
+        off = self.blk_off[:, :, :nb].cpu().numpy()
+        ln = self.blk_len[:, :, :nb].cpu().numpy()
+        pm = self.perm[:, :nb].cpu().numpy()
+        return off, ln, pm
+
+    def directory(self) -> List[BlockDirectoryEntry]:
+        """Directory entries in arena order (block-set, sequence, K heads, V heads)."""
+        o = self.owner
+        off, ln, pm = self.tables()
+        ents = []
+        for j in range(self.nblk_h):
+            for b in range(o.batch):
+                for kind in (KIND_K, KIND_V):
+                    for h in range(o.heads):
+                        u = b * o.heads + h
+                        ents.append(BlockDirectoryEntry(kind, self.layer, h, j * o.block, (j + 1) * o.block,
+                                                        int(off[kind, u, j]), int(ln[kind, u, j]),
+                                                        pm[b, j].astype(np.int64), b))
+        return ents
+
+    def block_bytes(self, e: BlockDirectoryEntry) -> bytes:
+        return bytes(self.arena[e.byte_offset:e.byte_offset + e.byte_len].cpu().numpy().tobytes())
+
+    def stream_bytes(self, seq: Optional[int] = 0) -> bytes:
+        """Blocks concatenated in directory order without alignment padding
+        (for one sequence this is byte-identical to the reference arena)."""
+        arena = self.arena[:max(1, int(self.tail.item()))].cpu().numpy()
+        out = bytearray()
+        for e in self.directory():
+            if seq is None or e.seq == seq:
+                out += arena[e.byte_offset:e.byte_offset + e.byte_len].tobytes()
+        return bytes(out)
+
+
+def ctypes_ref(s):
+    import ctypes
+    return ctypes.byref(s)
+
+
+class CompressedStore:
+    """SPEC.md:357-362.  Device-resident, batched, one sub-store per layer."""
+
+    def __init__(self, layers: int, heads: int, head_dim: int, batch: int = 1, rel_scale_k: float = 0.1,
+                 rel_scale_v: float = 0.2, pack_size: int = 16, repack: str = "none", block: int = 64,
+                 buffer: int = 128, device=None, max_tokens: Optional[int] = None, check: bool = True):
+        if repack not in REPACK_STRATEGIES:
+            raise ValueError(f"repack must be one of {REPACK_STRATEGIES}")
+        if pack_size not in (2, 4, 8, 16, 32):
+            raise ValueError("pack_size must be one of 2, 4, 8, 16, 32")
+        if block % pack_size or block > 256:
+            raise ValueError("block must be a multiple of pack_size and <= 256")
+        if repack != "none" and block > 64:
+            raise ValueError("repacking needs block <= 64")
+        if not (0 < rel_scale_k <= 1 and 0 < rel_scale_v <= 1):
+            raise ValueError("relative scales must be in (0, 1]")
+        if buffer < block:
+            raise ValueError("buffer must hold at least one block")
+        N.lib()  # fail loudly without the CUDA library / device
+        self.layers, self.heads, self.head_dim, self.batch = layers, heads, head_dim, batch
+        self.rel_scale_k, self.rel_scale_v = float(rel_scale_k), float(rel_scale_v)
+        self.pack_size, self.repack, self.block, self.buffer = pack_size, repack, block, buffer
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.check = check
+        init_blocks = max(4, math.ceil((max_tokens or 4096) / block))
+        self.layer_stores = [LayerStore(self, l, init_blocks) for l in range(layers)]
+
+    def __getitem__(self, layer: int) -> LayerStore:
+        if not (0 <= layer < self.layers):
+            raise IndexError(f"layer {layer} out of range [0, {self.layers})")
+        return self.layer_stores[layer]
+
+    def total_tokens(self, layer: int) -> int:
+        return self[layer].tokens
+
+    # normalisation of inputs to [B, T, H, D] fp16 on the device
+    def _norm(self, x, tokens_axis: bool) -> torch.Tensor:
+        if not isinstance(x, torch.Tensor):
+            x = torch.as_tensor(np.asarray(x))
+        H, D, B = self.heads, self.head_dim, self.batch
+        shape = tuple(x.shape)
+        if tokens_axis:
+            if x.dim() == 3 and B == 1 and shape[1:] == (H, D):
+                x = x.unsqueeze(0)
+            elif x.dim() == 2 and B == 1 and shape[1] == H * D:
+                x = x.reshape(1, shape[0], H, D)
+            if x.dim() != 4 or tuple(x.shape[:1]) != (B,) or tuple(x.shape[2:]) != (H, D):
+                raise E.ShapeMismatchError(f"expected [B={B}, T, H={H}, D={D}] tokens, got {shape}")
+        else:
+            if x.numel() != B * H * D:
+                raise E.ShapeMismatchError(f"expected {B}x{H}x{D} values per token, got {shape}")
+            x = x.reshape(B, 1, H, D)
+        if x.dtype != torch.float16:
+            x = x.to(torch.float16)
+        return x.to(self.device).contiguous()
+
+    def append_token(self, layer: int, k_vec, v_vec):
+        """SPEC.md:365-373."""
+        ls = self[layer]
+        k = self._norm(k_vec, False)
+        v = self._norm(v_vec, False)
+        ls.compress(k, v, self.check)
+
+    def compress_batch(self, layer: int, k_tokens, v_tokens):
+        """identical final state to appending token by token."""
+        ls = self[layer]
+        k = self._norm(k_tokens, True)
+        v = self._norm(v_tokens, True)
+        if k.shape != v.shape:
+            raise E.ShapeMismatchError("K and V batches differ in shape")
+        ls.compress(k, v, self.check)
+
+    def iterate_blocks(self, layer: int, kind: int, seq: int = 0):
+        """directory entries of (layer, kind) then the residue handle."""
+        ls = self[layer]
+        ents = [e for e in ls.directory() if e.kind == kind and e.seq == seq]
+        return ents + [ResidueHandle(layer, ls.nblk_h * self.block, ls.nres_h, seq)]
+
+    def check_errors(self):
+        for ls in self.layer_stores:
+            flags = int(ls.err.item())
+            if flags:
+                ls.err.zero_()
+                N.raise_flags(flags, f"layer {ls.layer}")
+
+    def snapshot_stats(self, include_staging: bool = False):
+        """exact byte counts and CR per (layer, kind)."""
+        out = {}
+        for ls in self.layer_stores:
+            _, ln, _ = ls.tables()
+            for kind in (KIND_K, KIND_V):
+                phys = int(ln[kind].astype(np.int64).sum())
+                nblocks = int(ln[kind].size)
+                logical = nblocks * self.block * self.head_dim * 2
+                res = ls.nres_h * self.batch * self.heads * self.head_dim * 2 if include_staging else 0
+                widths = None
+                out[(ls.layer, kind)] = {
+                    "blocks": nblocks, "bytes_physical": phys + res, "bytes_logical": logical + res,
+                    "cr": (logical + res) / (phys + res) if phys + res else None, "width_hist": widths,
+                }
+        return out
+
+
+def append_token(store: CompressedStore, layer: int, k_vec, v_vec):
+    store.append_token(layer, k_vec, v_vec)
+
+
+def compress_batch(store: CompressedStore, layer: int, k_tokens, v_tokens):
+    store.compress_batch(layer, k_tokens, v_tokens)
+
+
+def iterate_blocks(store: CompressedStore, layer: int, kind: int, seq: int = 0):
+    return store.iterate_blocks(layer, kind, seq)
+
+
+def snapshot_stats(store: CompressedStore, include_staging: bool = False):
+    return store.snapshot_stats(include_staging)

@@ -1,0 +1,321 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact: quantized codes, params, packed bytes, store streams, CR.
+Tolerance: fused GEMV outputs, ||gpu - f64 oracle||_inf <= 1e-3 * ||f64||_inf
+(SURVEY Appendix A #12)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import packkv_oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+def _pk():
+    import paper_2512_24449_b200 as pk
+    from paper_2512_24449_b200 import bitpack_codec as C, fused_kernels as F, quantizer as Q
+    from paper_2512_24449_b200.kv_store import CompressedStore
+    return pk, C, F, Q, CompressedStore
+
+
+def _close(a, ref):
+    a = np.asarray(a, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = max(np.abs(ref).max(), 1e-30)
+    err = np.abs(a - ref).max() if ref.size else 0.0
+    assert err <= TOL * scale, f"max abs err {err:.3e} > {TOL} * {scale:.3e}"
+    return err / scale
+
+
+# ------------------------------------------------------------------ quantizer
+@pytest.mark.parametrize("rel", [0.05, 0.1, 0.2, 0.5, 1.0, 0.0123])
+def test_quantize_bit_exact(rel):
+    _, _, _, Q, _ = _pk()
+    rng = np.random.default_rng(int(rel * 1000))
+    x = (rng.standard_normal((40, 64, 128)) * rng.uniform(0.001, 50, (40, 64, 1))).astype(np.float16)
+    x[0, 0, :] = 3.0                                     # constant row
+    x[1, 0, :3] = [0, 0.25, 1]                           # tie trap
+    qb = Q.quantize_token_wise(torch.from_numpy(x).cuda(), rel)
+    q = qb.q.cpu().numpy().astype(np.int64)
+    for i in range(40):
+        r = O.quantize_token_wise(x[i], rel)
+        assert np.array_equal(q[i], r.q), f"codes differ in block {i}"
+        assert np.array_equal(qb.scale[i].cpu().numpy(), r.scale)
+        assert np.array_equal(qb.zp[i].cpu().numpy(), r.zp)
+    d = Q.dequantize(qb).cpu().numpy()
+    for i in range(3):
+        r = O.quantize_token_wise(x[i], rel)
+        assert np.array_equal(d[i], O.dequantize(r.q, r.scale, r.zp))
+
+
+def test_quantize_examples_and_errors():
+    pk, _, _, Q, _ = _pk()
+    qb = Q.quantize_token_wise(torch.tensor([[0.0, 0.34, 1.0]], dtype=torch.float16).cuda(), 0.1)
+    assert qb.q.cpu().tolist() == [[0, 3, 10]]
+    with pytest.raises(pk.errors.NonFiniteValueError):
+        Q.quantize_token_wise(torch.tensor([[0.0, float("inf")]], dtype=torch.float16).cuda(), 0.1)
+    assert Q.max_abs_error(torch.full((4, 8), 2.0, dtype=torch.float16).cuda(), 0.1) == 0.0
+
+
+# ------------------------------------------------------------------ codec
+def _rand_codes(rng, rows, cols, maxw):
+    return rng.integers(0, 1 << maxw, (rows, cols)) if maxw else np.zeros((rows, cols), np.int64)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_encode_bit_exact(k, layout):
+    _, C, _, Q, _ = _pk()
+    rng = np.random.default_rng(k * 10 + layout)
+    for rows, cols in [(64, 128), (k, 5), (2 * k, 37), (128, 64)]:
+        n = 6
+        q = np.stack([_rand_codes(rng, rows, cols, int(rng.integers(0, 16))) for _ in range(n)])
+        q[0] = 0
+        q[1, 0, 0] = 32767                                # width 15
+        scale = rng.uniform(0.01, 2, (n, rows)).astype(np.float32)
+        zp = rng.uniform(-3, 3, (n, rows)).astype(np.float16).astype(np.float32)
+        qb = Q.QuantBlock(torch.from_numpy(q.astype(np.int32)).to(torch.uint16).cuda(),
+                          torch.from_numpy(scale).cuda(), torch.from_numpy(zp).cuda(), 0 if layout == 0 else 1)
+        blocks = C.encode_blocks(qb, k, layout)
+        for i in range(n):
+            ref = O.encode_block(O.QuantBlock(q[i], scale[i], zp[i], qb.kind), k, layout, qb.kind)
+            got = blocks[i].to_bytes()
+            assert got == ref, f"block {i} ({rows}x{cols}) differs"
+            assert C.compression_ratio(blocks[i]) == O.compression_ratio(ref)
+        dec = C.decode_blocks([C.PackedBlock.from_bytes(
+            O.encode_block(O.QuantBlock(q[i], scale[i], zp[i], 0), k, layout, 0)) for i in range(n)])
+        assert np.array_equal(dec.q.cpu().numpy().astype(np.int64), q)
+        pb = C.PackedBlock.from_bytes(O.encode_block(O.QuantBlock(q[2], scale[2], zp[2], 0), k, layout, 0))
+        P = (rows // k) * cols
+        for p in (0, P // 3, P - 1):
+            assert np.array_equal(C.decode_pack_at(pb, p).cpu().numpy().astype(np.int64),
+                                  O.decode_pack_at(pb.to_bytes(), p))
+
+
+def test_decode_malformed():
+    pk, C, _, _, _ = _pk()
+    q = np.arange(64 * 8).reshape(64, 8) % 7
+    good = O.encode_block(O.QuantBlock(q, np.ones(64, np.float32), np.zeros(64, np.float32)), 16)
+    for bad in (good[:-1], good + b"\0", bytes([0, 0, 7]) + good[3:]):
+        with pytest.raises(pk.errors.MalformedBlockError):
+            C.decode_block(C.PackedBlock.from_bytes(bad))
+    with pytest.raises(IndexError):
+        C.decode_pack_at(C.PackedBlock.from_bytes(good), 10 ** 6)
+
+
+def test_encode_width_overflow():
+    pk, C, _, Q, _ = _pk()
+    q = np.zeros((16, 4), np.int64)
+    q[0, 0] = 65535
+    qb = Q.QuantBlock(torch.from_numpy(q.astype(np.int32)).to(torch.uint16).cuda(),
+                      torch.ones(16).cuda(), torch.zeros(16).cuda())
+    with pytest.raises(pk.errors.WidthOverflowError):
+        C.encode_block(qb, 16)
+
+
+# ------------------------------------------------------------------ store
+def _kv(rng, T, H, D, batch=None):
+    shape = (T, H, D) if batch is None else (batch, T, H, D)
+    return rng.standard_normal(shape).astype(np.float16), rng.standard_normal(shape).astype(np.float16)
+
+
+@pytest.mark.parametrize("repack", ["none", "v_median", "greedy"])
+@pytest.mark.parametrize("k", [8, 16])
+def test_store_stream_bit_exact(repack, k):
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(1)
+    H, D = 4, 64
+    kk, vv = _kv(rng, 200, H, D)
+    ref = O.OracleStore(1, H, D, pack_size=k, repack=repack)
+    ref.compress_batch(0, kk, vv)
+    st = CS(1, H, D, pack_size=k, repack=repack)
+    st.compress_batch(0, kk[:70], vv[:70])
+    st.compress_batch(0, kk[70:], vv[70:])
+    assert st[0].stream_bytes(0) == ref.layer_stream(0)
+    got = [(e.kind, e.head, e.token_start, e.byte_len, e.permutation.tolist()) for e in st[0].directory()]
+    exp = [(e.kind, e.head, e.token_start, e.byte_len, e.permutation.tolist()) for e in ref.directory]
+    assert got == exp
+    assert st[0].nres_h == 200 - 3 * 64
+    assert np.array_equal(st[0].stage[0, :, :st[0].nres_h].permute(1, 0, 2).cpu().numpy(), ref.stage_k[0])
+
+
+def test_store_incremental_equals_batch_and_thresholds():
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(2)
+    H, D = 2, 128
+    kk, vv = _kv(rng, 300, H, D)
+    a = CS(1, H, D)
+    for t in range(63):
+        a.append_token(0, kk[t], vv[t])
+    assert a[0].nblk_h == 0 and a[0].nres_h == 63
+    a.append_token(0, kk[63], vv[63])
+    assert a[0].nblk_h == 1 and a[0].nres_h == 0
+    for t in range(64, 300):
+        a.append_token(0, kk[t], vv[t])
+    b = CS(1, H, D)
+    b.compress_batch(0, kk[:100], vv[:100])
+    assert b[0].nblk_h == 1 and b[0].nres_h == 36
+    b.compress_batch(0, kk[100:], vv[100:])
+    assert a[0].stream_bytes(0) == b[0].stream_bytes(0)
+    c = CS(1, H, D)
+    c.compress_batch(0, kk[:0], vv[:0])
+    assert c[0].tokens == 0
+
+
+def test_store_errors():
+    pk, _, _, _, CS = _pk()
+    st = CS(1, 2, 64)
+    with pytest.raises(pk.errors.ShapeMismatchError):
+        st.append_token(0, np.zeros(127, np.float16), np.zeros(128, np.float16))
+    bad = np.zeros((2, 64), np.float16)
+    bad[1, 3] = np.nan
+    with pytest.raises(pk.errors.NonFiniteValueError):
+        st.append_token(0, bad, np.zeros((2, 64), np.float16))
+    with pytest.raises(IndexError):
+        st.append_token(3, np.zeros((2, 64), np.float16), np.zeros((2, 64), np.float16))
+
+
+def test_store_growth():
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(3)
+    H, D = 2, 64
+    kk, vv = _kv(rng, 1000, H, D)
+    st = CS(1, H, D, max_tokens=64)
+    for i in range(0, 1000, 130):
+        st.compress_batch(0, kk[i:i + 130], vv[i:i + 130])
+    ref = O.OracleStore(1, H, D)
+    ref.compress_batch(0, kk, vv)
+    assert st[0].stream_bytes(0) == ref.layer_stream(0)
+
+
+# ------------------------------------------------------------------ fused
+def _oracle_per_seq(kk, vv, H, D, k, repack="none"):
+    ref = O.OracleStore(1, H, D, pack_size=k, repack=repack)
+    ref.compress_batch(0, kk, vv)
+    return ref
+
+
+@pytest.mark.parametrize("k", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("D", [64, 128])
+def test_fused_vs_oracle(k, D):
+    _, _, F, _, CS = _pk()
+    rng = np.random.default_rng(k + D)
+    H, T = 2, 64 * 5 + 17
+    kk, vv = _kv(rng, T, H, D)
+    ref = _oracle_per_seq(kk, vv, H, D, k)
+    st = CS(1, H, D, pack_size=k)
+    st.compress_batch(0, kk, vv)
+    for G in (1, 4, 8):
+        q = rng.standard_normal((1, H * G, D)).astype(np.float32)
+        w = rng.random((1, H * G, T)).astype(np.float32)
+        s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+        o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+        for hq in range(H * G):
+            _close(s[0, hq], O.naive_k_scores(ref, 0, hq // G, q[0, hq]))
+            _close(o[0, hq], O.naive_v_output(ref, 0, hq // G, w[0, hq]))
+
+
+def test_fused_spec_api_and_token_map():
+    _, _, F, _, CS = _pk()
+    rng = np.random.default_rng(5)
+    H, D, T = 2, 128, 150
+    kk, vv = _kv(rng, T, H, D)
+    ref = _oracle_per_seq(kk, vv, H, D, 16, "v_median")
+    st = CS(1, H, D, repack="v_median")
+    st.compress_batch(0, kk, vv)
+    q = rng.standard_normal(D).astype(np.float32)
+    sv = F.fused_k_scores(st, 0, 1, q)
+    rs, rmap = O.fused_k_scores(ref, 0, 1, q)
+    _close(sv.scores.cpu().numpy(), rs)
+    assert np.array_equal(sv.token_map.cpu().numpy(), rmap)
+    e = np.zeros(D, np.float32)
+    e[7] = 1
+    col = F.fused_k_scores(st, 0, 0, e).scores.cpu().numpy()
+    _close(col, O.fused_k_scores(ref, 0, 0, e)[0])
+    w = np.zeros(T, np.float32)
+    w[70] = 1
+    _close(F.fused_v_output(st, 0, 0, w).cpu().numpy(), O.fused_v_output(ref, 0, 0, w))
+    assert np.all(F.fused_v_output(st, 0, 1, np.zeros(T, np.float32)).cpu().numpy() == 0)
+    assert np.all(F.fused_k_scores(st, 0, 1, np.zeros(D, np.float32)).scores.cpu().numpy() == 0)
+
+
+def test_fused_batched_gqa_ragged_residue():
+    _, _, F, _, CS = _pk()
+    rng = np.random.default_rng(6)
+    B, H, D, G = 3, 2, 128, 4
+    T = 64 * 3 + 5
+    kk, vv = _kv(rng, T, H, D, batch=B)
+    st = CS(1, H, D, batch=B)
+    st.compress_batch(0, kk[:, :40], vv[:, :40])
+    st.compress_batch(0, kk[:, 40:], vv[:, 40:])
+    q = rng.standard_normal((B, H * G, D)).astype(np.float32)
+    w = rng.random((B, H * G, T)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+    for b in range(B):
+        ref = _oracle_per_seq(kk[b], vv[b], H, D, 16)
+        assert st[0].stream_bytes(b) == ref.layer_stream(0)
+        for hq in range(H * G):
+            _close(s[b, hq], O.naive_k_scores(ref, 0, hq // G, q[b, hq]))
+            _close(o[b, hq], O.naive_v_output(ref, 0, hq // G, w[b, hq]))
+
+
+def test_fused_v_deterministic_and_linear():
+    _, _, F, _, CS = _pk()
+    rng = np.random.default_rng(7)
+    H, D, T = 2, 128, 64 * 40 + 3
+    kk, vv = _kv(rng, T, H, D)
+    st = CS(1, H, D)
+    st.compress_batch(0, kk, vv)
+    w = torch.rand((1, H * 4, T)).cuda()
+    a = F.fused_v_output_batched(st, 0, w).clone()
+    b = F.fused_v_output_batched(st, 0, w)
+    assert torch.equal(a, b)
+    q1, q2 = torch.randn((2, 1, H * 4, D)).cuda()
+    s12 = F.fused_k_scores_batched(st, 0, q1 + q2)
+    s1 = F.fused_k_scores_batched(st, 0, q1).clone() + F.fused_k_scores_batched(st, 0, q2)
+    assert (s12 - s1).abs().max() <= TOL * s12.abs().max()
+
+
+def test_fused_large_property():
+    """Large context through the size-independent property: fused == GPU
+    decode-then-f64-GEMV (naive) on the same store (config-B-like unit)."""
+    _, _, F, _, CS = _pk()
+    from paper_2512_24449_b200.tensor_model import gauss_outlier
+    H, D, G, T = 2, 128, 4, 32768 + 21
+    kk = gauss_outlier((1, T, H, D), seed=1)
+    vv = gauss_outlier((1, T, H, D), n_outlier=1, seed=2)
+    st = CS(1, H, D, max_tokens=T)
+    st.compress_batch(0, kk, vv)
+    q = torch.randn((1, H * G, D), device="cuda")
+    w = torch.softmax(torch.randn((1, H * G, T), device="cuda"), -1)
+    s = F.fused_k_scores_batched(st, 0, q)
+    o = F.fused_v_output_batched(st, 0, w)
+    Kd = F.decode_layer(st, 0, 0).double()          # [H, L, D]
+    Vd = F.decode_layer(st, 0, 1).double()
+    for hq in range(H * G):
+        rk = Kd[hq // G] @ q[0, hq].double()
+        rv = w[0, hq].double() @ Vd[hq // G]
+        assert (s[0, hq].double() - rk).abs().max() <= TOL * rk.abs().max()
+        assert (o[0, hq].double() - rv).abs().max() <= TOL * rv.abs().max()
+    # quantization error of the dequantized cache stays within the SPEC bound
+    k32 = kk[0].permute(1, 0, 2).float()
+    tm = F.token_map(st, 0)[0]
+    err = (Kd.float() - k32[:, tm]).abs()
+    rng_row = k32.amax(-1) - k32.amin(-1)
+    assert bool((err <= (0.1 / 2) * rng_row[:, tm, None] * 1.001 + 2 ** -10).all())
+
+
+def test_attention_decode_singleton():
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import attention_decode
+    rng = np.random.default_rng(9)
+    st = CS(1, 2, 64)
+    k, v = _kv(rng, 1, 2, 64)
+    st.compress_batch(0, k, v)
+    out = attention_decode(st, 0, 1, rng.standard_normal(64)).cpu().numpy()
+    assert np.allclose(out, v[0, 1].astype(np.float32))
