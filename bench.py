@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the PackKV decode-time hot path on B200.
+
+Metric (BASELINE.json): fused decompress+GEMV K/V throughput in fp16-equivalent
+GB/s (SPEC.md:475 accounting: B*Hkv*L*D*2 bytes per kind per step), set next to
+cuBLAS fp16 GEMV (torch.matmul) on the uncompressed cache, plus the
+compression ratio.
+
+Workload at N=1 (BASELINE.json configs[1], "config B"): Llama-3-8B GQA layer,
+8 KV heads / 32 query heads, head_dim 128, 32768-token context, batch 8,
+synthetic Gaussian KV with injected outlier channels, codec
+rel_k 0.1 / rel_v 0.2, pack 16, block 64, repack none.
+
+A step = fused K scores for every query head + fused V output for every query
+head over the whole compressed cache of the layer (all inputs resident in
+HBM); at N > 1 every rank owns its own (sequence, kv-head) shard of the same
+size (weak scaling) and the per-head outputs are all-gathered over NCCL.
+The per-step working set (~230 MB of compressed blocks) exceeds the 126 MB L2.
+
+`--impl reference` times the reference algorithm's CPU path (the numpy
+restatement of SPEC.md in oracle/, the reference ships no runnable code) on a
+bounded sample of the same workload with all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused decompress+GEMV K/V GB/s-equiv vs cuBLAS fp16 GEMV; compression ratio"
+UNIT = "GB/s (fp16-equivalent)"
+
+CONFIGS = {
+    # key: (batch, kv_heads, q_heads, head_dim, tokens, description)
+    "A": (1, 32, 32, 128, 4096, "Llama-2-7B single layer, MHA 32x128, 4K tokens, batch 1"),
+    "B": (8, 8, 32, 128, 32768, "Llama-3-8B GQA (8 kv / 32 q heads), 32K context, batch 8, 1 layer"),
+    "D": (8, 52, 52, 128, 32768, "LLaMA-30B shape (52 heads x 128), 32K context, batch 8, 1 layer"),
+    "E": (16, 8, 64, 128, 131072, "Llama-3-70B GQA (8 kv / 64 q heads), 128K context, batch 16, 1 layer"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        rs = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": rs,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def _cpu_unit(args):
+    """One (sequence, kv-head) unit through the CPU oracle: compress (untimed),
+    then the SPEC per-head fused K and V calls for its G query heads (timed)."""
+    seed, L, D, G = args
+    import numpy as np
+    from oracle import packkv_oracle as O
+    rng = np.random.default_rng(seed)
+    K = O.gen_gauss_outlier(rng, L, D, max(1, D * 4 // 128))[:, None, :]
+    V = O.gen_gauss_outlier(rng, L, D, max(1, D // 128))[:, None, :]
+    st = O.OracleStore(1, 1, D)
+    st.compress_batch(0, K, V)
+    q = rng.standard_normal((G, D)).astype(np.float32)
+    t0 = time.perf_counter()
+    for g in range(G):
+        s, _ = O.fused_k_scores(st, 0, 0, q[g])
+        w = O.softmax64(s / math.sqrt(D)).astype(np.float32)
+        O.fused_v_output(st, 0, 0, w)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, units: int, L: int, steps: int = 1):
+    """Times the oracle (kind "port") on `units` units of L tokens, one process per unit."""
+    import multiprocessing as mp
+    B, Hkv, Hq, D, _, _ = cfg
+    G = Hq // Hkv
+    cores = min(units, len(os.sched_getaffinity(0)))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        times = []
+        for s in range(steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_unit, [(1000 * s + u, L, D, G) for u in range(units)])
+            times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    logical = units * 2 * L * D * 2
+    return {"value": logical / t / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{units} (sequence, kv-head) units x {L} tokens, G={G} query heads each, "
+                      f"SPEC per-head fused_k_scores + fused_v_output (oracle/packkv_oracle.py, numpy), "
+                      f"{units} processes", "seconds_per_step": t}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    B, Hkv, Hq, D, L, desc = cfg
+    units = min(len(os.sched_getaffinity(0)), B * Hkv)
+    Ls = min(L, 8192)
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_baseline(cfg, units, 1024, 1)
+    cb = cpu_baseline(cfg, units, Ls, max(1, min(args.steps, 5)))
+    line = {"impl": "reference", "metric": METRIC, "value": round(cb["value"], 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config {args.config}: {desc}", "sample_tokens_per_unit": Ls,
+                       "sample_units": units},
+            "cpu_baseline": cb, "e2e": {"value": round(cb["value"], 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def build_store(cfg, rank, repack="none", chunk=4096):
+    import torch
+    from paper_2512_24449_b200.kv_store import CompressedStore
+    from paper_2512_24449_b200.tensor_model import gauss_outlier
+    B, Hkv, Hq, D, L, _ = cfg
+    st = CompressedStore(1, Hkv, D, batch=B, repack=repack, max_tokens=L, check=False)
+    for t0 in range(0, L, chunk):
+        T = min(chunk, L - t0)
+        k = gauss_outlier((B, T, Hkv, D), n_outlier=4, seed=17 + 7919 * rank + t0)
+        v = gauss_outlier((B, T, Hkv, D), n_outlier=1, seed=29 + 7919 * rank + t0)
+        st.compress_batch(0, k, v)
+    torch.cuda.synchronize()
+    st.check_errors()
+    return st
+
+
+def cublas_baseline(cfg, rank, reps=10):
+    """torch.matmul fp16 (fp32 accumulate) GEMV on the uncompressed cache."""
+    import torch
+    from paper_2512_24449_b200.tensor_model import gauss_outlier
+    B, Hkv, Hq, D, L, _ = cfg
+    G = Hq // Hkv
+    U = B * Hkv
+    Kf = torch.empty((U, L, D), dtype=torch.float16, device="cuda")
+    Vf = torch.empty((U, L, D), dtype=torch.float16, device="cuda")
+    for t0 in range(0, L, 4096):
+        T = min(4096, L - t0)
+        Kf[:, t0:t0 + T] = gauss_outlier((B, T, Hkv, D), 4, seed=17 + 7919 * rank + t0).permute(0, 2, 1, 3).reshape(U, T, D)
+        Vf[:, t0:t0 + T] = gauss_outlier((B, T, Hkv, D), 1, seed=29 + 7919 * rank + t0).permute(0, 2, 1, 3).reshape(U, T, D)
+    q = torch.randn((U, D, G), device="cuda").half()
+    w = torch.softmax(torch.randn((U, G, L), device="cuda"), -1).half()
+    res = {}
+    for name, fn in (("k", lambda: torch.matmul(Kf, q)), ("v", lambda: torch.matmul(w, Vf))):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res[name + "_us"] = statistics.median(ts) * 1e3
+    del Kf, Vf
+    torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2512_24449_b200 import fused_kernels as F
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+
+    cfg = CONFIGS[args.config]
+    B, Hkv, Hq, D, L, desc = cfg
+    G = Hq // Hkv
+    st = build_store(cfg, rank)
+    ls = st[0]
+    _, ln, _ = ls.tables()
+    phys_k = int(ln[0].astype(np.int64).sum())
+    phys_v = int(ln[1].astype(np.int64).sum())
+    nblocks_k = int(ln[0].size)
+    logical_kind = B * Hkv * L * D * 2
+    cr_k_wire, cr_v_wire = logical_kind / phys_k, logical_kind / phys_v
+    cr_k = B * Hkv * (L // 64) * 64 * D * 2 / (phys_k - 8 * nblocks_k)
+    cr_v = B * Hkv * (L // 64) * 64 * D * 2 / (phys_v - 8 * nblocks_k)
+    res_bytes = B * Hkv * ls.nres_h * D * 2
+    alg_k = phys_k + res_bytes + B * Hq * D * 4 + B * Hq * L * 4
+    alg_v = phys_v + res_bytes + B * Hq * L * 4 + B * Hq * D * 4
+
+    q = torch.randn((B, Hq, D), device="cuda")
+    scores = torch.empty((B, Hq, L), device="cuda")
+    out = torch.empty((B, Hq, D), device="cuda")
+    F.fused_k_scores_batched(st, 0, q, out=scores)
+    w = torch.softmax(scores / math.sqrt(D), -1).contiguous()
+    gathered = torch.empty((world * B, Hq, D), device="cuda") if world > 1 else None
+
+    def step():
+        F.fused_k_scores_batched(st, 0, q, out=scores)
+        F.fused_v_output_batched(st, 0, w, out=out)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out)
+
+    for _ in range(args.warmup):
+        step()
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    with sampler:
+        e_start = torch.cuda.Event(enable_timing=True)
+        e_end = torch.cuda.Event(enable_timing=True)
+        e_start.record()
+        for i in range(K):
+            evs[i][0].record()
+            F.fused_k_scores_batched(st, 0, q, out=scores)
+            evs[i][1].record()
+            F.fused_v_output_batched(st, 0, w, out=out)
+            evs[i][2].record()
+            if world > 1:
+                dist.all_gather_into_tensor(gathered, out)
+        e_end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e_start.elapsed_time(e_end) / K
+    k_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    v_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    t = torch.tensor([ms, k_ms, v_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, k_ms, v_ms = (float(x) for x in t.tolist())
+    value = world * 2 * logical_kind / (ms * 1e-3) / 1e9
+
+    # ---- e2e through the public API: host q -> attention_decode -> host out
+    q_host = torch.randn((B, Hq, D)).pin_memory()
+    out_host = torch.empty((B, Hq, D)).pin_memory()
+
+    def e2e_step():
+        qd = q_host.to("cuda", non_blocking=True)
+        o = attention_decode_batched(st, 0, qd)
+        out_host.copy_(o, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(K):
+        e2e_step()
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([a0.elapsed_time(a1) / K], device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+    e2e_value = world * 2 * logical_kind / (e2e_ms * 1e-3) / 1e9
+
+    peak, peak_src = load_peaks()
+    dom = "k" if k_ms >= v_ms else "v"
+    dom_ms = k_ms if dom == "k" else v_ms
+    alg = alg_k if dom == "k" else alg_v
+    achieved = alg / (dom_ms * 1e-3) / 1e9
+    traffic = load_traffic().get(f"{args.config}_{dom}")
+
+    cub = None
+    if not args.no_cublas:
+        del scores
+        cub = cublas_baseline(cfg, rank)
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg, units=min(8, len(os.sched_getaffinity(0))), L=min(L, 32768), steps=1)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8->f32", "data": "synthetic gaussian + outlier channels (BASELINE.md §3)",
+            "config": {"workload": f"config {args.config}: {desc}", "batch": B, "kv_heads": Hkv, "q_heads": Hq,
+                       "head_dim": D, "tokens": L, "layers": 1, "rel_k": 0.1, "rel_v": 0.2, "pack_size": 16,
+                       "block": 64, "repack": "none", "parallelism": f"(batch, kv-head) shards x{world}",
+                       "l2": "per-step working set (compressed K+V blocks) exceeds the 126 MB L2"},
+            "compression_ratio": {"k": round(cr_k, 4), "v": round(cr_v, 4), "k_wire": round(cr_k_wire, 4),
+                                  "v_wire": round(cr_v_wire, 4)},
+            "kernels": {"fused_k_us": round(k_ms * 1e3, 2), "fused_v_us": round(v_ms * 1e3, 2),
+                        "fused_k_gbs_equiv": round(logical_kind / (k_ms * 1e-3) / 1e9, 1),
+                        "fused_v_gbs_equiv": round(logical_kind / (v_ms * 1e-3) / 1e9, 1),
+                        "fused_k_gbs_physical": round(alg_k / (k_ms * 1e-3) / 1e9, 1),
+                        "fused_v_gbs_physical": round(alg_v / (v_ms * 1e-3) / 1e9, 1)},
+            "roofline": {"bound": "hbm", "kernel": f"fused_{dom}", "achieved": round(achieved, 1), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "algorithmic_bytes_per_launch": alg},
+            "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": B * Hq * D * 4,
+                    "d2h_bytes_per_step": B * Hq * D * 4,
+                    "path": "attention_decode_batched (public API): H2D q, fused K, softmax, fused V, D2H out",
+                    "ms_per_step": round(e2e_ms, 5)},
+            "gpu_launches": 3 * K,
+            "clocks": sampler.summary(),
+        }
+        if cub:
+            line["cublas"] = {"k_us": round(cub["k_us"], 2), "v_us": round(cub["v_us"], 2),
+                              "k_gbs_equiv": round(logical_kind / (cub["k_us"] * 1e-6) / 1e9, 1),
+                              "v_gbs_equiv": round(logical_kind / (cub["v_us"] * 1e-6) / 1e9, 1),
+                              "speedup_k": round(cub["k_us"] / (k_ms * 1e3), 3),
+                              "speedup_v": round(cub["v_us"] / (v_ms * 1e3), 3)}
+        if cb:
+            line["cpu_baseline"] = cb
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -136,7 +136,8 @@ def decode_blocks(blocks: Sequence[PackedBlock]) -> QuantBlock:
     q = torch.empty((n, rows, cols), dtype=torch.uint16, device=dev)
     params = torch.zeros((n, rows, 2), dtype=torch.float32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
-    N.check(N.lib().pkv_decode(N.ptr(buf), N.ptr(offs.to(dev)), N.ptr(lens.to(dev)), n, rows, cols, N.ptr(q),
+    offs_d, lens_d = offs.to(dev), lens.to(dev)     # keep alive across the async launch
+    N.check(N.lib().pkv_decode(N.ptr(buf), N.ptr(offs_d), N.ptr(lens_d), n, rows, cols, N.ptr(q),
                                N.ptr(params), N.ptr(err), N.stream()), "decode_block")
     N.raise_flags(int(err.item()), "decode_block")
     return QuantBlock(q, params[..., 0], params[..., 1], blocks[0].kind, 0.0)

@@ -166,8 +166,11 @@ __device__ inline int64_t encode_block_dev(const EncSrc& src, const Fmt& f, int 
       s = src.params[2 * sr];
       z = src.params[2 * sr + 1];
     }
-    const uint16_t s16 = __half_as_ushort(__float2half_rn(s));
-    const uint16_t z16 = __half_as_ushort(__float2half_rn(z));
+    // Move the f16 bit patterns through a 32-bit integer register: without the
+    // asm barrier ptxas folds "cvt.f16 then st.u8" into a numeric F2I.U8.
+    uint32_t s16 = __half_as_ushort(__float2half_rn(s));
+    uint32_t z16 = __half_as_ushort(__float2half_rn(z));
+    asm volatile("" : "+r"(s16), "+r"(z16));
     if ((s16 & 0x7c00) == 0x7c00) ovf = true;  // scale not representable in f16
     uint8_t* pp = sbuf + f.par_off + 4 * r;
     pp[0] = uint8_t(s16 & 0xff);
