@@ -206,8 +206,8 @@ def cublas_baseline(cfg, rank, reps=10):
     Vf = torch.empty((U, L, D), dtype=torch.float16, device="cuda")
     for t0 in range(0, L, 4096):
         T = min(4096, L - t0)
-        Kf[:, t0:t0 + T] = gauss_outlier((B, T, Hkv, D), 4, seed=17 + 7919 * rank + t0).permute(0, 2, 1, 3).reshape(U, T, D)
-        Vf[:, t0:t0 + T] = gauss_outlier((B, T, Hkv, D), 1, seed=29 + 7919 * rank + t0).permute(0, 2, 1, 3).reshape(U, T, D)
+        Kf[:, t0:t0 + T] = gauss_outlier((B, T, Hkv, D), n_outlier=4, seed=17 + 7919 * rank + t0).permute(0, 2, 1, 3).reshape(U, T, D)
+        Vf[:, t0:t0 + T] = gauss_outlier((B, T, Hkv, D), n_outlier=1, seed=29 + 7919 * rank + t0).permute(0, 2, 1, 3).reshape(U, T, D)
     q = torch.randn((U, D, G), device="cuda").half()
     w = torch.softmax(torch.randn((U, G, L), device="cuda"), -1).half()
     res = {}
