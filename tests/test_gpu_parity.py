@@ -320,3 +320,28 @@ def test_attention_decode_singleton():
     st.compress_batch(0, k, v)
     out = attention_decode(st, 0, 1, rng.standard_normal(64)).cpu().numpy()
     assert np.allclose(out, v[0, 1].astype(np.float32))
+
+
+@pytest.mark.parametrize("rels", [(0.1, 0.2), (0.02, 0.05), (0.0004, 0.01)])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_fused_default_format_paths(rels, G):
+    """k=16, D=128 runs the tensor-core kernels; wide packs (w > 5) and codes
+    above 2047 exercise their in-launch scalar path."""
+    _, _, F, _, CS = _pk()
+    rng = np.random.default_rng(int(G * 100 + rels[0] * 1e4))
+    H, D, T = 3, 128, 64 * 7 + 9
+    kk = (rng.standard_normal((T, H, D)) * rng.uniform(0.1, 4, (T, 1, 1))).astype(np.float16)
+    vv = rng.standard_normal((T, H, D)).astype(np.float16)
+    ref = O.OracleStore(1, H, D, rel_k=rels[0], rel_v=rels[1])
+    ref.compress_batch(0, kk, vv)
+    st = CS(1, H, D, rel_scale_k=rels[0], rel_scale_v=rels[1])
+    st.compress_batch(0, kk[:100], vv[:100])
+    st.compress_batch(0, kk[100:], vv[100:])
+    assert st[0].stream_bytes(0) == ref.layer_stream(0)
+    q = rng.standard_normal((1, H * G, D)).astype(np.float32)
+    w = rng.standard_normal((1, H * G, T)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+    for hq in range(H * G):
+        _close(s[0, hq], O.naive_k_scores(ref, 0, hq // G, q[0, hq]))
+        _close(o[0, hq], O.naive_v_output(ref, 0, hq // G, w[0, hq]))
