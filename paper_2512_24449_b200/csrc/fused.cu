@@ -23,13 +23,12 @@
 
 using namespace pkv;
 
-// tensor-core path for the default format (fused_mma.cu)
-bool pkv_mma_supported(const pkv_layer_t* L, int G, int64_t stride);
-int pkv_mma_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
-                    cudaStream_t s);
-int64_t pkv_mma_v_scratch(const pkv_layer_t* L, int nblocks, int G);
-int pkv_mma_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
-                    float* part, cudaStream_t s);
+// int8 tensor-core path for the default format (fused_i8.cu)
+bool pkv_i8_supported(const pkv_layer_t* L, int G, int64_t stride);
+int pkv_i8_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
+                   cudaStream_t s);
+int pkv_i8_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
+                   float* part, cudaStream_t s);
 
 namespace {
 
@@ -369,8 +368,8 @@ extern "C" int pkv_fused_k_scores(const pkv_layer_t* L, int32_t nblocks, const f
     return PKV_E_SHAPE;
   }
   cudaStream_t strm = (cudaStream_t)stream;
-  if (pkv_mma_supported(L, G, score_stride) && (reinterpret_cast<uintptr_t>(q) & 15) == 0)
-    return pkv_mma_fused_k(L, nblocks, q, G, scores, score_stride, strm);
+  if (pkv_i8_supported(L, G, score_stride) && (reinterpret_cast<uintptr_t>(q) & 15) == 0)
+    return pkv_i8_fused_k(L, nblocks, q, G, scores, score_stride, strm);
   PKV_DISPATCH_KD(L->pack_size, L->head_dim, return (launch_k<KPc, Dc>(L, nblocks, q, G, scores, score_stride, strm)));
   return PKV_OK;
 }
@@ -394,8 +393,8 @@ extern "C" int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const f
   }
   cudaStream_t strm = (cudaStream_t)stream;
   float* part = (float*)scratch;
-  if (pkv_mma_supported(L, G, w_stride) && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
-    return pkv_mma_fused_v(L, nblocks, w, G, w_stride, out, part, strm);
+  if (pkv_i8_supported(L, G, w_stride) && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
+    return pkv_i8_fused_v(L, nblocks, w, G, w_stride, out, part, strm);
   if (G <= 4) {
     PKV_DISPATCH_KD(L->pack_size, L->head_dim,
                     return (launch_v<KPc, Dc, 4>(L, nblocks, w, G, w_stride, out, part, strm)));
