@@ -29,6 +29,7 @@ int pkv_i8_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, flo
                    cudaStream_t s);
 int pkv_i8_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
                    float* part, cudaStream_t s);
+int64_t pkv_i8_v_scratch(const pkv_layer_t* L, int nblocks, int G);
 
 namespace {
 
@@ -378,7 +379,9 @@ extern "C" int64_t pkv_fused_v_scratch_bytes(const pkv_layer_t* L, int32_t nbloc
   int G = 0;
   if (fused_args(L, nblocks, q_heads, &G)) return -1;
   const int nsplit = max(1, (nblocks + kBpc - 1) / kBpc);
-  return int64_t(L->batch) * L->heads * nsplit * G * (L->head_dim + 1) * 4;
+  const int64_t v1 = int64_t(L->batch) * L->heads * nsplit * G * (L->head_dim + 1) * 4;
+  const int64_t i8 = pkv_i8_supported(L, G, 4) ? pkv_i8_v_scratch(L, nblocks, G) : 0;
+  return v1 > i8 ? v1 : i8;
 }
 
 extern "C" int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const float* w, int32_t q_heads,

@@ -104,6 +104,14 @@ __device__ __forceinline__ void imma_uu0(int (&d)[4], const uint32_t (&a)[4], ui
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0));
 }
 
+// D = A(u8) * B(s8), C = 0
+__device__ __forceinline__ void imma_us0(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%10,%10,%10};\n"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0));
+}
+
 __device__ __forceinline__ float h2f(uint32_t bits16) { return __half2float(__ushort_as_half(uint16_t(bits16))); }
 
 // byte `p` (runtime 0..3) of each of x0..x3 packed into one register
@@ -158,12 +166,21 @@ __device__ __forceinline__ bool parse_block(const uint8_t* __restrict__ blk, int
   return __all_sync(PKV_FULL, ok);
 }
 
+// a*b + c forced onto the FMA pipe (IMAD), keeping the ALU pipe for byte work
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 // Four fields at stride w (w <= 4) in the low bits of x -> one byte each,
-// plus the pack minimum: exact uint8 codes (byte e = field e).
-__device__ __forceinline__ uint32_t spread4(uint32_t x, uint32_t s1, uint32_t s2, uint32_t m4, uint32_t mr) {
-  const uint32_t y = __byte_perm(x, x << s1, 0x7610);  // fields 0,1 low half; 2,3 high half
-  const uint32_t z = __byte_perm(y, y << s2, 0x7250);  // one field per byte
-  return (z & m4) + mr;
+// plus the pack minimum: exact uint8 codes (byte e = field e).  Left shifts
+// are multiplies by M1 = 2^(16-2w) / M2 = 2^(8-w) (FMA pipe); the byte
+// permutes and the mask stay on the ALU pipe.
+__device__ __forceinline__ uint32_t spread4(uint32_t x, uint32_t M1, uint32_t M2, uint32_t m4, uint32_t mr) {
+  const uint32_t y = __byte_perm(x, x * M1, 0x7610);  // fields 0,1 low half; 2,3 high half
+  const uint32_t z = __byte_perm(y, y * M2, 0x7250);  // one field per byte
+  return imad(z & m4, 1u, mr);
 }
 
 // All 16 fields of the pack described by `d` (w <= 4) as uint8 codes:
@@ -173,16 +190,16 @@ __device__ __forceinline__ void decode16(const uint32_t* __restrict__ words, uin
   const uint32_t w = (d >> 18) & 15u;
   const uint32_t* p = words + (bo >> 5);
   const uint32_t w0 = p[0], w1 = p[1], w2 = p[2];
-  const uint32_t xlo = __funnelshift_r(w0, w1, bo);
-  const uint32_t xmid = __funnelshift_r(w1, w2, bo);
-  const uint32_t xhi = __funnelshift_rc(xlo, xmid, 8u * w);  // fields 8..15 (clamped at 32 for w = 4)
-  const uint32_t m4 = (0x01010101u << w) - 0x01010101u;
+  const uint32_t xlo = __funnelshift_r(w0, w1, bo);   // payload bits 0..31
+  const uint32_t xmid = __funnelshift_r(w1, w2, bo);  // payload bits 32..63
+  const uint32_t M2 = 256u >> w, M1 = M2 * M2, M3 = M1 * M1;  // 2^(8-w), 2^(16-2w), 2^(32-4w)
+  const uint32_t xhi = __funnelshift_rc(xlo, xmid, w * 8u);    // fields 8..15
+  const uint32_t m4 = imad(0x01010101u, 1u << w, 0u - 0x01010101u);
   const uint32_t mr = (d >> 22) * 0x01010101u;
-  const uint32_t s2 = 8u - w, s1 = 2u * s2, s3 = 4u * w;
-  r[0] = spread4(xlo, s1, s2, m4, mr);
-  r[1] = spread4(xlo >> s3, s1, s2, m4, mr);
-  r[2] = spread4(xhi, s1, s2, m4, mr);
-  r[3] = spread4(xhi >> s3, s1, s2, m4, mr);
+  r[0] = spread4(xlo, M1, M2, m4, mr);
+  r[1] = spread4(__umulhi(xlo, M3), M1, M2, m4, mr);  // x >> 4w on the FMA pipe
+  r[2] = spread4(xhi, M1, M2, m4, mr);
+  r[3] = spread4(__umulhi(xhi, M3), M1, M2, m4, mr);
 }
 
 // Generic scalar field read (any width <= 15) from a block at any alignment.
@@ -198,13 +215,20 @@ __device__ __forceinline__ uint32_t pack_min(const uint8_t* __restrict__ blk, in
 }
 
 // ---------------------------------------------------------------- ring
+// Persistent CTAs: work item = (unit, split of <= kBpc blocks); CTA c owns items
+// c, c + gridDim.x, ...  The producer warp streams the blocks of all its items
+// back to back through the byte ring (tickets are global across items), so the
+// ring never drains at item boundaries.
 struct Ring {
   uint8_t* data;
   uint64_t* full;
   uint64_t* empty;
   uint32_t* start;  // [kTickets] ring offset of each ticket's block
   uint32_t* abs;    // [kTickets] producer-private absolute start
+  int64_t* soff;    // [kBpc] producer-private block offsets of the current item
+  int* slen;        // [kBpc]
 };
+constexpr size_t kRingBytes = kRing + kTickets * 16 + kTickets * 8 + kBpc * 12;
 
 __device__ __forceinline__ uint8_t* setup_ring(uint8_t* smem, Ring& R) {
   R.data = smem;
@@ -212,6 +236,8 @@ __device__ __forceinline__ uint8_t* setup_ring(uint8_t* smem, Ring& R) {
   R.empty = R.full + kTickets;
   R.start = (uint32_t*)(R.empty + kTickets);
   R.abs = R.start + kTickets;
+  R.soff = (int64_t*)(R.abs + kTickets);
+  R.slen = (int*)(R.soff + kBpc);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTickets; ++s) {
       mbar_init(&R.full[s], 1);
@@ -219,35 +245,61 @@ __device__ __forceinline__ uint8_t* setup_ring(uint8_t* smem, Ring& R) {
     }
     fence_barrier_init();
   }
-  return (uint8_t*)(R.abs + kTickets);
+  return smem + kRingBytes;
 }
-constexpr size_t kRingBytes = kRing + kTickets * 8 * 2 + kTickets * 4 * 2;
 
-// Single-lane producer: block i -> ticket i % kTickets, placed back to back in
-// the byte ring; waits (in ticket order) for releases when out of tickets or bytes.
-__device__ void produce(const Ring& R, const pkv_layer_t& L, int64_t tab, int j0, int nb) {
+struct Item {
+  int u, s, b, h, j0, nb, nbk;
+};
+__device__ __forceinline__ Item item_of(const pkv_layer_t& L, int item, int nsplit) {
+  Item it;
+  it.u = item / nsplit;
+  it.s = item - it.u * nsplit;
+  it.b = it.u / L.heads;
+  it.h = it.u - it.b * L.heads;
+  it.nbk = L.nblk[it.b];
+  it.j0 = it.s * kBpc;
+  it.nb = max(0, min(kBpc, it.nbk - it.j0));
+  return it;
+}
+
+// Producer warp: for every item of this CTA, stage its block table in smem
+// (warp-parallel), then one lane issues the TMA copies.
+__device__ void produce(const Ring& R, const pkv_layer_t& L, int kind, int nsplit, int nitems, int lane) {
+  const int U = L.batch * L.heads;
   uint32_t head = 0;
-  int oldest = 0;
-  for (int i = 0; i < nb; ++i) {
-    const int j = j0 + i;
-    const int64_t off = L.blk_off[tab + j];
-    const uint32_t bytes = uint32_t((L.blk_len[tab + j] + 15) & ~15);
-    const uint32_t size = bytes + 16;  // +16: slack for the decoders' word over-reads
-    uint32_t pos = head % kRing;
-    if (pos + size > kRing) {
-      head += kRing - pos;
-      pos = 0;
+  int oldest = 0, ticket = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const Item it = item_of(L, item, nsplit);
+    const int64_t tab = (int64_t(kind) * U + it.u) * L.max_blocks + it.j0;
+    if (lane < it.nb) {
+      R.soff[lane] = L.blk_off[tab + lane];
+      R.slen[lane] = L.blk_len[tab + lane];
     }
-    while (oldest < i && ((i - oldest) >= kTickets || head + size - R.abs[oldest % kTickets] > kRing)) {
-      mbar_wait(&R.empty[oldest % kTickets], uint32_t((oldest / kTickets) & 1));
-      ++oldest;
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = 0; i < it.nb; ++i, ++ticket) {
+        const uint32_t bytes = uint32_t((R.slen[i] + 15) & ~15);
+        const uint32_t size = bytes + 16;  // +16: slack for the decoders' word over-reads
+        uint32_t pos = head % kRing;
+        if (pos + size > kRing) {
+          head += kRing - pos;
+          pos = 0;
+        }
+        while (oldest < ticket &&
+               ((ticket - oldest) >= kTickets || head + size - R.abs[oldest % kTickets] > kRing)) {
+          mbar_wait(&R.empty[oldest % kTickets], uint32_t((oldest / kTickets) & 1));
+          ++oldest;
+        }
+        const int tk = ticket % kTickets;
+        R.abs[tk] = head;
+        R.start[tk] = pos;
+        mbar_expect_tx(&R.full[tk], bytes);
+        tma_load_1d(R.data + pos, L.arena + R.soff[i], bytes, &R.full[tk]);
+        head += size;
+      }
     }
-    const int tk = i % kTickets;
-    R.abs[tk] = head;
-    R.start[tk] = pos;
-    mbar_expect_tx(&R.full[tk], bytes);
-    tma_load_1d(R.data + pos, L.arena + off, bytes, &R.full[tk]);
-    head += size;
+    __syncwarp();
   }
 }
 
@@ -255,115 +307,55 @@ __device__ void produce(const Ring& R, const pkv_layer_t& L, int64_t tab, int j0
 // k-step ks of a block: k-slot 4t+e <-> (row-group t, token 8ks+e),
 // 4t+16+e <-> (row-group t, token 8ks+4+e).  Lane (gi, tq) decodes whole packs
 // of row-group tq and feeds tokens 0-7 to ks = 0 and 8-15 to ks = 1.
+// B = digits of x_t = rint(w_t * s_t * f), f a power of two chosen per block
+// and head so |x| <= 2^22; the int32 tile sums of each block are converted to
+// f32 (divided by f) into per-lane float accumulators.
 template <int NU>  // NU = unsigned digit tiles: 1 for G <= 4, 2 for G <= 8
 __global__ void __launch_bounds__(kThreads) fused_v_i8_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
-                                                               int64_t wstride, float* __restrict__ part, int bpc,
-                                                               int nsplit) {
+                                                               int64_t wstride, float* __restrict__ part, int nsplit,
+                                                               int nitems, float* __restrict__ vscr) {
   extern __shared__ __align__(128) uint8_t smem[];
   Ring R;
   uint8_t* rest = setup_ring(smem, R);
   uint32_t* desc_all = (uint32_t*)rest;                 // [kCW][512]
-  float* vslow = (float*)(desc_all + kCW * 512);        // [kCW][8][kD] scalar-path partials
-  float* sf = vslow + kCW * 8 * kD;                     // [8] fixed-point scale per head
-  float* szs = sf + 8;                                  // [8] sum_t w*z per head
-  float* red_w = szs + 8;                               // [kCW][8]
-  float* red_s = red_w + kCW * 8;                       // [kCW]
-  float* red_z = red_s + kCW;                           // [kCW][8]
+  float* red = (float*)(desc_all + kCW * 512);          // [kCW][8][kD]
+  float* zred = red + kCW * 8 * kD;                     // [kCW][8]
+  int* touched = (int*)(zred + kCW * 8);                // [kCW]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gi = lane >> 2, tq = lane & 3;
-  const int u = blockIdx.y, b = u / L.heads, h = u % L.heads, U = L.batch * L.heads;
-  const int Hq = L.heads * G;
-  const int nbk = L.nblk[b];
-  const int j0 = blockIdx.x * bpc, j1 = min(nbk, j0 + bpc);
-  const int nb = max(0, j1 - j0);
-  const int64_t tab = (int64_t(1) * U + u) * L.max_blocks;
-  const float* wu = w + (int64_t(b) * Hq + int64_t(h) * G) * wstride;
-  for (int e = threadIdx.x; e < kCW * 8 * kD; e += blockDim.x) vslow[e] = 0.f;
+  const int U = L.batch * L.heads;
+  if (threadIdx.x < kCW) touched[threadIdx.x] = 0;
   __syncthreads();
-
-  if (warp == kCW) {
-    if (lane == 0) produce(R, L, tab, j0, nb);
+  if (warp == kCW) {  // producer; no CTA-wide barrier follows
+    produce(R, L, 1, nsplit, nitems, lane);
+    return;
   }
 
-  int accU[NU][8][4];
-  int accS[8][4];
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      accS[mt][e] = 0;
-#pragma unroll
-      for (int nu = 0; nu < NU; ++nu) accU[nu][mt][e] = 0;
-    }
-  }
+  uint32_t* desc = desc_all + warp * 512;
+  float* vsl = vscr + (int64_t(blockIdx.x) * kCW + warp) * (8 * kD);  // scalar-path partials
+  const int gA = gi >> 1, gB = 4 + (gi >> 1);
+  const uint32_t selU = uint32_t(gi & 1) | (uint32_t(4 + (gi & 1)) << 4);
+  const uint32_t selS = 2u | (6u << 4);
+  const bool odd = gi & 1;
+  int ticket_base = 0;
 
-  if (warp < kCW) {
-    // ---- pre-pass over the CTA's tokens (4 per step): max|w| per head, max scale, sum w*z
-    const int tid = threadIdx.x;
-    float wm[8], zs[8], smax = 0.f;
+#pragma unroll 1
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const Item it = item_of(L, item, nsplit);
+    const int Hq = L.heads * G;
+    const float* wu = w + (int64_t(it.b) * Hq + int64_t(it.h) * G) * wstride;
+    float accF[NU][8][2];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) wm[g] = zs[g] = 0.f;
-    for (int t4 = tid; t4 < nb * (kRows / 4); t4 += kCW * 32) {
-      const int t = 4 * t4, j = j0 + t / kRows, r = t % kRows;
-      const uint2* pp = (const uint2*)(L.arena + L.blk_off[tab + j] + kPar + 4 * r);
-      const uint2 p01 = pp[0], p23 = pp[1];
-      const float s4[4] = {h2f(p01.x & 0xffff), h2f(p01.y & 0xffff), h2f(p23.x & 0xffff), h2f(p23.y & 0xffff)};
-      const float z4[4] = {h2f(p01.x >> 16), h2f(p01.y >> 16), h2f(p23.x >> 16), h2f(p23.y >> 16)};
-      smax = fmaxf(smax, fmaxf(fmaxf(fabsf(s4[0]), fabsf(s4[1])), fmaxf(fabsf(s4[2]), fabsf(s4[3]))));
+    for (int nu = 0; nu < NU; ++nu)
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        if (g < G) {
-          const float4 wv = *(const float4*)(wu + int64_t(g) * wstride + int64_t(j) * kRows + r);
-          wm[g] = fmaxf(wm[g], fmaxf(fmaxf(fabsf(wv.x), fabsf(wv.y)), fmaxf(fabsf(wv.z), fabsf(wv.w))));
-          zs[g] = fmaf(wv.x, z4[0], fmaf(wv.y, z4[1], fmaf(wv.z, z4[2], fmaf(wv.w, z4[3], zs[g]))));
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      smax = fmaxf(smax, __shfl_xor_sync(PKV_FULL, smax, o));
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        wm[g] = fmaxf(wm[g], __shfl_xor_sync(PKV_FULL, wm[g], o));
-        zs[g] += __shfl_xor_sync(PKV_FULL, zs[g], o);
-      }
-    }
-    if (lane == 0) {
-      red_s[warp] = smax;
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        red_w[warp * 8 + g] = wm[g];
-        red_z[warp * 8 + g] = zs[g];
-      }
-    }
-    consumer_sync();
-    if (threadIdx.x < 8) {
-      const int g = threadIdx.x;
-      float m = 0.f, zz = 0.f, sm = 0.f;
-      for (int wv = 0; wv < kCW; ++wv) {
-        m = fmaxf(m, red_w[wv * 8 + g]);
-        zz += red_z[wv * 8 + g];
-        sm = fmaxf(sm, red_s[wv]);
-      }
-      const float v = m * sm;
-      // |w * s * f| <= 2^22 so the 3-byte two's complement digits are exact
-      float f = 1.f;
-      if (v > 0.f) f = exp2f(fminf(fmaxf(floorf(log2f(4194304.f / v)), -120.f), 120.f));
-      sf[g] = f;
-      szs[g] = zz;
-    }
-    consumer_sync();
+      for (int mt = 0; mt < 8; ++mt) accF[nu][mt][0] = accF[nu][mt][1] = 0.f;
+    float zacc[NU] = {};
+    bool slow_used = false;
 
-    // ---- main loop: this warp owns blocks warp, warp + kCW, ...
-    uint32_t* desc = desc_all + warp * 512;
-    float* vsl = vslow + warp * 8 * kD;
-    const int gA = gi >> 1, gB = 4 + (gi >> 1);
-    const float fA = sf[gA], fB = sf[gB];
-    const uint32_t selU = uint32_t(gi & 1) | (uint32_t(4 + (gi & 1)) << 4);
-    const uint32_t selS = 2u | (6u << 4);
-    const bool odd = gi & 1;
-    for (int i = warp; i < nb; i += kCW) {
-      const int tk = i % kTickets;
-      const int j = j0 + i;
+#pragma unroll 1
+    for (int i = warp; i < it.nb; i += kCW) {
+      const int t = ticket_base + i;
+      const int tk = t % kTickets;
+      const int j = it.j0 + i;
       // weights of this lane's 16 tokens (row-group tq), issued before the wait
       float wa[16], wb[16];
       {
@@ -378,27 +370,47 @@ __global__ void __launch_bounds__(kThreads) fused_v_i8_kernel(pkv_layer_t L, con
           wb[4 * q] = vb.x; wb[4 * q + 1] = vb.y; wb[4 * q + 2] = vb.z; wb[4 * q + 3] = vb.w;
         }
       }
-      mbar_wait(&R.full[tk], uint32_t((i / kTickets) & 1));
+      mbar_wait(&R.full[tk], uint32_t((t / kTickets) & 1));
       const uint8_t* blk = R.data + R.start[tk];
       const uint32_t* words = (const uint32_t*)blk;
+      // w*s and w*z for the lane's tokens
+      float mA = 0.f, mB = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint2 pr = *(const uint2*)(blk + kPar + 4 * (16 * tq + 2 * q));
+        const float s0 = h2f(pr.x & 0xffff), s1 = h2f(pr.y & 0xffff);
+        const float z0 = h2f(pr.x >> 16), z1 = h2f(pr.y >> 16);
+        if (!odd) {  // one lane per (head, row-group) adds the z term
+          zacc[0] = fmaf(wa[2 * q], z0, fmaf(wa[2 * q + 1], z1, zacc[0]));
+          if (NU == 2) zacc[NU - 1] = fmaf(wb[2 * q], z0, fmaf(wb[2 * q + 1], z1, zacc[NU - 1]));
+        }
+        wa[2 * q] *= s0;
+        wa[2 * q + 1] *= s1;
+        mA = fmaxf(mA, fmaxf(fabsf(wa[2 * q]), fabsf(wa[2 * q + 1])));
+        if (NU == 2) {
+          wb[2 * q] *= s0;
+          wb[2 * q + 1] *= s1;
+          mB = fmaxf(mB, fmaxf(fabsf(wb[2 * q]), fabsf(wb[2 * q + 1])));
+        }
+      }
+      // block max per head: lanes (gi, tq) with the same gi >> 1
+#pragma unroll
+      for (int o = 1; o <= 4; o <<= 1) {
+        mA = fmaxf(mA, __shfl_xor_sync(PKV_FULL, mA, o));
+        if (NU == 2) mB = fmaxf(mB, __shfl_xor_sync(PKV_FULL, mB, o));
+      }
+      const float fA = mA > 0.f ? exp2f(fminf(floorf(log2f(4194304.f / mA)), 120.f)) : 1.f;
+      const float fB = mB > 0.f ? exp2f(fminf(floorf(log2f(4194304.f / mB)), 120.f)) : 1.f;
       const bool fast = parse_block(blk, lane, desc);
       if (fast) {
-        // B digits of x_t = rint(w_t * s_t * f) for the lane's 16 tokens
         uint32_t bu[NU][2][2], bs[2][2];
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
           uint32_t xa[8], xb[8];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int tok = 16 * tq + 8 * ks + 2 * q;
-            const uint2 pr = *(const uint2*)(blk + kPar + 4 * tok);
-            const float s0 = h2f(pr.x & 0xffff), s1 = h2f(pr.y & 0xffff);
-            xa[2 * q] = uint32_t(__float2int_rn(wa[8 * ks + 2 * q] * fA * s0));
-            xa[2 * q + 1] = uint32_t(__float2int_rn(wa[8 * ks + 2 * q + 1] * fA * s1));
-            if (NU == 2) {
-              xb[2 * q] = uint32_t(__float2int_rn(wb[8 * ks + 2 * q] * fB * s0));
-              xb[2 * q + 1] = uint32_t(__float2int_rn(wb[8 * ks + 2 * q + 1] * fB * s1));
-            }
+          for (int e = 0; e < 8; ++e) {
+            xa[e] = uint32_t(__float2int_rn(wa[8 * ks + e] * fA));
+            if (NU == 2) xb[e] = uint32_t(__float2int_rn(wb[8 * ks + e] * fB));
           }
           bu[0][ks][0] = gather_byte(xa[0], xa[1], xa[2], xa[3], selU);
           bu[0][ks][1] = gather_byte(xa[4], xa[5], xa[6], xa[7], selU);
@@ -409,27 +421,55 @@ __global__ void __launch_bounds__(kThreads) fused_v_i8_kernel(pkv_layer_t L, con
             bs[ks][0] = gather_byte(odd ? xb[0] : xa[0], odd ? xb[1] : xa[1], odd ? xb[2] : xa[2], odd ? xb[3] : xa[3], selS);
             bs[ks][1] = gather_byte(odd ? xb[4] : xa[4], odd ? xb[5] : xa[5], odd ? xb[6] : xa[6], odd ? xb[7] : xa[7], selS);
           } else {
-            // S tile: column 2t -> head t (digit 2), 2t+1 -> zero
             bs[ks][0] = odd ? 0u : gather_byte(xa[0], xa[1], xa[2], xa[3], selS);
             bs[ks][1] = odd ? 0u : gather_byte(xa[4], xa[5], xa[6], xa[7], selS);
           }
         }
+        // inverse scales of the heads this lane's D columns belong to (head tq, tq + 4)
+        const float inv0 = 1.f / __shfl_sync(PKV_FULL, fA, (2 * tq) << 2);
+        const float inv1 = NU == 2 ? 1.f / __shfl_sync(PKV_FULL, fB, (2 * tq) << 2) : 0.f;
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
           const int c = 16 * mt + gi;
           uint32_t P[4], Q[4];
           decode16(words, desc[tq * 128 + c], P);
           decode16(words, desc[tq * 128 + c + 8], Q);
+          int dU[NU][4], dS[4];
+          {
+            const uint32_t a[4] = {P[0], Q[0], P[1], Q[1]};
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint32_t a[4] = {P[2 * ks], Q[2 * ks], P[2 * ks + 1], Q[2 * ks + 1]};
+            for (int nu = 0; nu < NU; ++nu) imma_uu0(dU[nu], a, bu[nu][0][0], bu[nu][0][1]);
+            imma_us0(dS, a, bs[0][0], bs[0][1]);
+          }
+          {
+            const uint32_t a[4] = {P[2], Q[2], P[3], Q[3]};
 #pragma unroll
-            for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu][mt], a, bu[nu][ks][0], bu[nu][ks][1]);
-            imma_us(accS[mt], a, bs[ks][0], bs[ks][1]);
+            for (int nu = 0; nu < NU; ++nu) imma_uu(dU[nu], a, bu[nu][1][0], bu[nu][1][1]);
+            imma_us(dS, a, bs[1][0], bs[1][1]);
+          }
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            accF[0][mt][half] = fmaf(float(dU[0][2 * half]) + 256.f * float(dU[0][2 * half + 1]) +
+                                         65536.f * float(dS[2 * half]), inv0, accF[0][mt][half]);
+            if (NU == 2)
+              accF[NU - 1][mt][half] = fmaf(float(dU[NU - 1][2 * half]) + 256.f * float(dU[NU - 1][2 * half + 1]) +
+                                                65536.f * float(dS[2 * half + 1]), inv1, accF[NU - 1][mt][half]);
           }
         }
       } else {
-        // scalar path: lane owns channels lane + 32q, all 64 tokens, all heads
+        // scalar path (rare): lane owns channels lane + 32q, all 64 tokens, all heads;
+        // partials accumulate in this warp's global scratch (fixed order, deterministic)
+        if (!slow_used) {
+          for (int e = lane; e < 8 * kD; e += 32) vsl[e] = 0.f;
+          __syncwarp();
+          slow_used = true;
+        }
+        float acc[8][4];
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[g][q] = vsl[g * kD + lane + 32 * q];
+#pragma unroll 1
         for (int r = 0; r < kRows; ++r) {
           const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * r);
           const float s = h2f(pr & 0xffff);
@@ -444,67 +484,63 @@ __global__ void __launch_bounds__(kThreads) fused_v_i8_kernel(pkv_layer_t L, con
             const uint32_t wd = (d >> 18) & 15u;
             const float code = float(pack_min(blk, rg * 128 + c) + field_bytes(blk, (d & 0x3ffffu) + tt * wd, wd));
 #pragma unroll
-            for (int g = 0; g < 8; ++g) vsl[g * kD + c] = fmaf(ws[g], code, vsl[g * kD + c]);
+            for (int g = 0; g < 8; ++g) acc[g][q] = fmaf(ws[g], code, acc[g][q]);
           }
         }
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) vsl[g * kD + lane + 32 * q] = acc[g][q];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&R.empty[tk]);
     }
-  }
+    ticket_base += it.nb;
 
-  // ---- cross-warp reduction (fixed order), after every consumer finished
-  __syncthreads();
-  float* red = (float*)smem;  // [kCW][8][kD] (reuses the ring)
-  if (warp < kCW) {
-    const float* vsl = vslow + warp * 8 * kD;
+    // ---- item epilogue: fixed-order cross-warp reduction
+#pragma unroll
+    for (int nu = 0; nu < NU; ++nu) {
+      zacc[nu] += __shfl_xor_sync(PKV_FULL, zacc[nu], 1);
+      zacc[nu] += __shfl_xor_sync(PKV_FULL, zacc[nu], 2);
+    }
+    consumer_sync();  // previous item's readers of red are done
 #pragma unroll
     for (int g = 0; g < 8; ++g)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) red[(warp * 8 + g) * kD + lane + 32 * q] = vsl[g * kD + lane + 32 * q];
-  }
-  __syncthreads();
-  if (warp < kCW) {
+      for (int q = 0; q < 4; ++q) red[(warp * 8 + g) * kD + lane + 32 * q] = slow_used ? vsl[g * kD + lane + 32 * q] : 0.f;
+    if (tq == 0 && !odd) {
+      zred[warp * 8 + gA] = zacc[0];
+      if (NU == 2) zred[warp * 8 + gB] = zacc[NU - 1];
+    }
+    if (tq == 0 && odd && NU == 1) zred[warp * 8 + 4 + gA] = 0.f;
+    if (NU == 1 && lane < 4) zred[warp * 8 + 4 + lane] = 0.f;
+    __syncwarp();
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         const int c = 16 * mt + gi + 8 * half;
-        // tile U0: cols 2tq, 2tq+1 = head tq digits 0, 1; tile S col 2tq = head tq digit 2
-        {
-          const int g = tq;
-          if (g < G) {
-            const double v = double(accU[0][mt][2 * half]) + 256.0 * double(accU[0][mt][2 * half + 1]) +
-                             65536.0 * double(accS[mt][2 * half]);
-            red[(warp * 8 + g) * kD + c] += float(v / double(sf[g]));
-          }
-        }
-        if (NU == 2) {
-          const int g = tq + 4;
-          if (g < G) {
-            const double v = double(accU[NU - 1][mt][2 * half]) + 256.0 * double(accU[NU - 1][mt][2 * half + 1]) +
-                             65536.0 * double(accS[mt][2 * half + 1]);
-            red[(warp * 8 + g) * kD + c] += float(v / double(sf[g]));
-          }
-        }
+        red[(warp * 8 + tq) * kD + c] += accF[0][mt][half];
+        if (NU == 2) red[(warp * 8 + tq + 4) * kD + c] += accF[NU - 1][mt][half];
       }
     }
-  }
-  __syncthreads();
-  const int nr = (blockIdx.x == 0) ? L.nres[b] : 0;
-  const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
-  for (int e = threadIdx.x; e < G * (kD + 1); e += blockDim.x) {
-    const int g = e / (kD + 1), c = e % (kD + 1);
-    float s = 0.f;
-    if (c < kD) {
+    consumer_sync();
+    const int nr = (it.s == 0) ? L.nres[it.b] : 0;
+    const uint16_t* vr = L.stage + (int64_t(1) * U + it.u) * L.buffer * kD;
+    for (int e = threadIdx.x; e < G * (kD + 1); e += kCW * 32) {
+      const int g = e / (kD + 1), c = e % (kD + 1);
+      float sum = 0.f;
+      if (c < kD) {
 #pragma unroll
-      for (int wv = 0; wv < kCW; ++wv) s += red[(wv * 8 + g) * kD + c];
-      const float* wr = wu + int64_t(g) * wstride + int64_t(nbk) * kRows;
-      for (int t = 0; t < nr; ++t) s = fmaf(wr[t], __half2float(__ushort_as_half(vr[t * kD + c])), s);
-    } else {
-      s = szs[g];
+        for (int wv = 0; wv < kCW; ++wv) sum += red[(wv * 8 + g) * kD + c];
+        const float* wr = wu + int64_t(g) * wstride + int64_t(it.nbk) * kRows;
+        for (int t = 0; t < nr; ++t) sum = fmaf(wr[t], __half2float(__ushort_as_half(vr[t * kD + c])), sum);
+      } else {
+#pragma unroll
+        for (int wv = 0; wv < kCW; ++wv) sum += zred[wv * 8 + g];
+      }
+      part[((int64_t(it.u) * nsplit + it.s) * G + g) * (kD + 1) + c] = sum;
     }
-    part[((int64_t(u) * nsplit + blockIdx.x) * G + g) * (kD + 1) + c] = s;
   }
 }
 
@@ -544,7 +580,8 @@ __device__ __forceinline__ int kslot_pos(int m, int slot) {
 
 template <int NU>
 __global__ void __launch_bounds__(kThreads) fused_k_i8_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
-                                                               float* __restrict__ scores, int64_t sstride, int bpc) {
+                                                               float* __restrict__ scores, int64_t sstride,
+                                                               int nsplit, int nitems) {
   extern __shared__ __align__(128) uint8_t smem[];
   Ring R;
   uint8_t* rest = setup_ring(smem, R);
@@ -552,66 +589,13 @@ __global__ void __launch_bounds__(kThreads) fused_k_i8_kernel(pkv_layer_t L, con
   float* sq = (float*)(desc_all + kCW * 512);  // [8][kD]
   float* sqsum = sq + 8 * kD;                  // [8]
   float* sfq = sqsum + 8;                      // [8]
+  uint32_t* sbq = (uint32_t*)(sfq + 8);        // [8][NU+1][32] query digit fragments
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gi = lane >> 2, tq = lane & 3;
-  const int u = blockIdx.y, b = u / L.heads, h = u % L.heads, U = L.batch * L.heads;
-  const int Hq = L.heads * G;
-  const int nbk = L.nblk[b];
-  const int j0 = blockIdx.x * bpc, j1 = min(nbk, j0 + bpc);
-  const int nb = max(0, j1 - j0);
-  const int64_t tab = (int64_t(0) * U + u) * L.max_blocks;
-  float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride;
-  const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
-  for (int e = threadIdx.x; e < 8 * kD; e += blockDim.x) sq[e] = (e / kD) < G ? qu[e] : 0.f;
-  __syncthreads();
-
-  if (warp < kCW) {
-    for (int g = warp; g < 8; g += kCW) {
-      float s = 0.f, m = 0.f;
-      for (int c = lane; c < kD; c += 32) {
-        s += sq[g * kD + c];
-        m = fmaxf(m, fabsf(sq[g * kD + c]));
-      }
-      s = warp_sum(s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(PKV_FULL, m, o));
-      if (lane == 0) {
-        sqsum[g] = s;
-        sfq[g] = m > 0.f ? exp2f(fminf(fmaxf(floorf(log2f(4194304.f / m)), -120.f), 120.f)) : 1.f;
-      }
-    }
-  }
+  const int U = L.batch * L.heads;
   __syncthreads();
   if (warp == kCW) {  // producer; no CTA-wide barrier follows
-    if (lane == 0) produce(R, L, tab, j0, nb);
+    produce(R, L, 0, nsplit, nitems, lane);
     return;
-  }
-
-  // query digit fragments (B of the compute IMMA): col gi of tile U = (head gi/2, digit gi&1),
-  // tile S col 2t = (head t, digit 2), col 2t+1 = (head t+4, digit 2) or zero
-  uint32_t bqu[NU][4][2], bqs[4][2];
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      uint32_t xu[NU][4], xs[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int c = kpos_to_col(kslot_pos(m, 4 * tq + 16 * r + e), kD);
-#pragma unroll
-        for (int nu = 0; nu < NU; ++nu) {
-          const int g = 4 * nu + (gi >> 1);
-          const int xi = __float2int_rn(sq[g * kD + c] * sfq[g]);
-          xu[nu][e] = (uint32_t(xi) >> (8 * (gi & 1))) & 0xffu;
-        }
-        const int gs = (gi >> 1) + 4 * (gi & 1);
-        const bool use = (gi & 1) == 0 || NU == 2;
-        const int xi = __float2int_rn(sq[gs * kD + c] * sfq[gs]);
-        xs[e] = use ? ((uint32_t(xi) >> 16) & 0xffu) : 0u;
-      }
-#pragma unroll
-      for (int nu = 0; nu < NU; ++nu) bqu[nu][m][r] = xu[nu][0] | (xu[nu][1] << 8) | (xu[nu][2] << 16) | (xu[nu][3] << 24);
-      bqs[m][r] = xs[0] | (xs[1] << 8) | (xs[2] << 16) | (xs[3] << 24);
-    }
   }
   // transposition permutations: A1 for selects (0,1) and (2,3)
   uint32_t ap[2][4];
@@ -625,105 +609,194 @@ __global__ void __launch_bounds__(kThreads) fused_k_i8_kernel(pkv_layer_t L, con
                   (perm_byte(row, kb + 2, 2 * sb) << 16) | (perm_byte(row, kb + 3, 2 * sb) << 24);
     }
   }
-  const float qs0 = sqsum[tq], fq0 = sfq[tq];
-  const float qs1 = sqsum[(tq + 4) & 7], fq1 = sfq[(tq + 4) & 7];
-
   uint32_t* desc = desc_all + warp * 512;
-  for (int i = warp; i < nb; i += kCW) {
-    const int tk = i % kTickets;
-    const int j = j0 + i;
-    mbar_wait(&R.full[tk], uint32_t((i / kTickets) & 1));
-    const uint8_t* blk = R.data + R.start[tk];
-    const uint32_t* words = (const uint32_t*)blk;
-    const bool fast = parse_block(blk, lane, desc);
-    if (fast) {
+  const int tid = threadIdx.x;
+  // query of the first item (next items are prefetched into registers)
+  float qn[8];
+  auto load_q = [&](int item) {
+    const Item it = item_of(L, item, nsplit);
+    const float* qu = q + (int64_t(it.b) * L.heads * G + int64_t(it.h) * G) * kD;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = tid + k * kCW * 32;
+      qn[k] = (e / kD) < G ? qu[e] : 0.f;
+    }
+  };
+  if (blockIdx.x < nitems) load_q(blockIdx.x);
+  int ticket_base = 0;
+
 #pragma unroll 1
-      for (int rg = 0; rg < 4; ++rg) {
-        int accU[NU][4], accS[4];
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const Item it = item_of(L, item, nsplit);
+    const int Hq = L.heads * G;
+    float* srow = scores + (int64_t(it.b) * Hq + int64_t(it.h) * G) * sstride;
+    consumer_sync();  // every consumer is done with the previous item's query
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          accS[e] = 0;
-#pragma unroll
-          for (int nu = 0; nu < NU; ++nu) accU[nu][e] = 0;
-        }
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          uint32_t P[4];
-          decode16(words, desc[rg * 128 + 32 * m + 8 * tq + gi], P);
-          int d[4][4];  // [token half a/b][select pair lo/hi]
-          imma_uu0(d[0], ap[0], P[0], P[1]);  // tokens 0-7, selects 0/1
-          imma_uu0(d[1], ap[1], P[0], P[1]);  // tokens 0-7, selects 2/3
-          imma_uu0(d[2], ap[0], P[2], P[3]);  // tokens 8-15, selects 0/1
-          imma_uu0(d[3], ap[1], P[2], P[3]);  // tokens 8-15, selects 2/3
-          uint32_t a[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            a[t] = uint32_t(d[(t & 1) * 2 + (t >> 1)][0]) | (uint32_t(d[(t & 1) * 2 + (t >> 1)][1]) << 8) |
-                   (uint32_t(d[(t & 1) * 2 + (t >> 1)][2]) << 16) | (uint32_t(d[(t & 1) * 2 + (t >> 1)][3]) << 24);
-#pragma unroll
-          for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, bqu[nu][m][0], bqu[nu][m][1]);
-          imma_us(accS, a, bqs[m][0], bqs[m][1]);
-        }
-        const int tA = 16 * rg + gi, tB = tA + 8;
-        const uint32_t pA = *(const uint32_t*)(blk + kPar + 4 * tA);
-        const uint32_t pB = *(const uint32_t*)(blk + kPar + 4 * tB);
-        const float sA = h2f(pA & 0xffff), zA = h2f(pA >> 16), sB = h2f(pB & 0xffff), zB = h2f(pB >> 16);
-        if (tq < G) {
-          const float vA = float(accU[0][0]) + 256.f * float(accU[0][1]) + 65536.f * float(accS[0]);
-          const float vB = float(accU[0][2]) + 256.f * float(accU[0][3]) + 65536.f * float(accS[2]);
-          srow[int64_t(tq) * sstride + int64_t(j) * kRows + tA] = fmaf(sA, vA / fq0, zA * qs0);
-          srow[int64_t(tq) * sstride + int64_t(j) * kRows + tB] = fmaf(sB, vB / fq0, zB * qs0);
-        }
-        if (NU == 2 && tq + 4 < G) {
-          const float vA = float(accU[NU - 1][0]) + 256.f * float(accU[NU - 1][1]) + 65536.f * float(accS[1]);
-          const float vB = float(accU[NU - 1][2]) + 256.f * float(accU[NU - 1][3]) + 65536.f * float(accS[3]);
-          srow[int64_t(tq + 4) * sstride + int64_t(j) * kRows + tA] = fmaf(sA, vA / fq1, zA * qs1);
-          srow[int64_t(tq + 4) * sstride + int64_t(j) * kRows + tB] = fmaf(sB, vB / fq1, zB * qs1);
-        }
+    for (int k = 0; k < 8; ++k) sq[tid + k * kCW * 32] = qn[k];
+    consumer_sync();
+    if (item + int(gridDim.x) < nitems) load_q(item + gridDim.x);  // prefetch the next item's query
+    for (int g = warp; g < 8; g += kCW) {
+      float sm = 0.f, m = 0.f;
+      for (int c = lane; c < kD; c += 32) {
+        sm += sq[g * kD + c];
+        m = fmaxf(m, fabsf(sq[g * kD + c]));
       }
-    } else {
-      // scalar path: lane computes tokens lane and lane+32 for every head
-      for (int half = 0; half < 2; ++half) {
-        const int t = lane + 32 * half, rg = t >> 4, tt = t & 15;
-        float acc[8];
+      sm = warp_sum(sm);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) acc[g] = 0.f;
-        for (int pos = 0; pos < 128; ++pos) {
-          const uint32_t d = desc[rg * 128 + pos];
-          const uint32_t wd = (d >> 18) & 15u;
-          const float code = float(pack_min(blk, rg * 128 + pos) + field_bytes(blk, (d & 0x3ffffu) + tt * wd, wd));
-          const int c = kpos_to_col(pos, kD);
-#pragma unroll
-          for (int g = 0; g < 8; ++g) acc[g] = fmaf(code, sq[g * kD + c], acc[g]);
-        }
-        const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * t);
-        const float s = h2f(pr & 0xffff), z = h2f(pr >> 16);
-        for (int g = 0; g < G; ++g) srow[int64_t(g) * sstride + int64_t(j) * kRows + t] = fmaf(s, acc[g], z * sqsum[g]);
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(PKV_FULL, m, o));
+      if (lane == 0) {
+        sqsum[g] = sm;
+        sfq[g] = m > 0.f ? exp2f(fminf(fmaxf(floorf(log2f(4194304.f / m)), -120.f), 120.f)) : 1.f;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&R.empty[tk]);
-  }
+    consumer_sync();
+    // query digit fragments (B of the compute IMMA), built once per item in shared
+    // memory by all consumer threads: col gi of tile U = (head gi/2, digit gi&1),
+    // tile S col 2t = (head t, digit 2), col 2t+1 = (head t+4, digit 2) or zero
+#pragma unroll 1
+    for (int e = tid; e < 8 * (NU + 1) * 32; e += kCW * 32) {
+      const int ln = e & 31, idx = e >> 5, tt = idx % (NU + 1), mr = idx / (NU + 1);
+      const int m = mr >> 1, r = mr & 1, lgi = ln >> 2, ltq = ln & 3;
+      uint32_t v = 0;
+#pragma unroll 1
+      for (int ee = 0; ee < 4; ++ee) {
+        const int c = kpos_to_col(kslot_pos(m, 4 * ltq + 16 * r + ee), kD);
+        uint32_t byte;
+        if (tt < NU) {
+          const int g = 4 * tt + (lgi >> 1);
+          byte = (uint32_t(__float2int_rn(sq[g * kD + c] * sfq[g])) >> (8 * (lgi & 1))) & 0xffu;
+        } else {
+          const int gs = (lgi >> 1) + 4 * (lgi & 1);
+          const bool use = (lgi & 1) == 0 || NU == 2;
+          byte = use ? (uint32_t(__float2int_rn(sq[gs * kD + c] * sfq[gs])) >> 16) & 0xffu : 0u;
+        }
+        v |= byte << (8 * ee);
+      }
+      sbq[e] = v;
+    }
+    consumer_sync();
+    uint32_t bqu[NU][4][2], bqs[4][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+#pragma unroll
+        for (int nu = 0; nu < NU; ++nu) bqu[nu][m][r] = sbq[((m * 2 + r) * (NU + 1) + nu) * 32 + lane];
+        bqs[m][r] = sbq[((m * 2 + r) * (NU + 1) + NU) * 32 + lane];
+      }
+    const float qs0 = sqsum[tq], fq0 = 1.f / sfq[tq];
+    const float qs1 = sqsum[(tq + 4) & 7], fq1 = 1.f / sfq[(tq + 4) & 7];
 
-  if (blockIdx.x == 0) {  // uncompressed residue, same launch
-    const int nr = L.nres[b];
-    const uint16_t* kr = L.stage + (int64_t(0) * U + u) * L.buffer * kD;
-    for (int t = warp; t < nr; t += kCW) {
-      for (int g = 0; g < G; ++g) {
-        float a = 0.f;
-        for (int c = lane; c < kD; c += 32) a = fmaf(__half2float(__ushort_as_half(kr[t * kD + c])), sq[g * kD + c], a);
-        a = warp_sum(a);
-        if (lane == 0) srow[int64_t(g) * sstride + int64_t(nbk) * kRows + t] = a;
+#pragma unroll 1
+    for (int i = warp; i < it.nb; i += kCW) {
+      const int t = ticket_base + i;
+      const int tk = t % kTickets;
+      const int j = it.j0 + i;
+      mbar_wait(&R.full[tk], uint32_t((t / kTickets) & 1));
+      const uint8_t* blk = R.data + R.start[tk];
+      const uint32_t* words = (const uint32_t*)blk;
+      const bool fast = parse_block(blk, lane, desc);
+      if (fast) {
+#pragma unroll 1
+        for (int rg = 0; rg < 4; ++rg) {
+          int accU[NU][4], accS[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            accS[e] = 0;
+#pragma unroll
+            for (int nu = 0; nu < NU; ++nu) accU[nu][e] = 0;
+          }
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            uint32_t P[4];
+            decode16(words, desc[rg * 128 + 32 * m + 8 * tq + gi], P);
+            int d[4][4];  // [token half a/b][select pair lo/hi]
+            imma_uu0(d[0], ap[0], P[0], P[1]);  // tokens 0-7, selects 0/1
+            imma_uu0(d[1], ap[1], P[0], P[1]);  // tokens 0-7, selects 2/3
+            imma_uu0(d[2], ap[0], P[2], P[3]);  // tokens 8-15, selects 0/1
+            imma_uu0(d[3], ap[1], P[2], P[3]);  // tokens 8-15, selects 2/3
+            uint32_t a[4];
+#pragma unroll
+            for (int x4 = 0; x4 < 4; ++x4) {
+              const int x = (x4 & 1) * 2 + (x4 >> 1);
+              a[x4] = uint32_t(d[x][0]) | (uint32_t(d[x][1]) << 8) | (uint32_t(d[x][2]) << 16) | (uint32_t(d[x][3]) << 24);
+            }
+#pragma unroll
+            for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, bqu[nu][m][0], bqu[nu][m][1]);
+            imma_us(accS, a, bqs[m][0], bqs[m][1]);
+          }
+          const int tA = 16 * rg + gi, tB = tA + 8;
+          const uint32_t pA = *(const uint32_t*)(blk + kPar + 4 * tA);
+          const uint32_t pB = *(const uint32_t*)(blk + kPar + 4 * tB);
+          const float sA = h2f(pA & 0xffff), zA = h2f(pA >> 16), sB = h2f(pB & 0xffff), zB = h2f(pB >> 16);
+          if (tq < G) {
+            const float vA = float(accU[0][0]) + 256.f * float(accU[0][1]) + 65536.f * float(accS[0]);
+            const float vB = float(accU[0][2]) + 256.f * float(accU[0][3]) + 65536.f * float(accS[2]);
+            srow[int64_t(tq) * sstride + int64_t(j) * kRows + tA] = fmaf(sA, vA * fq0, zA * qs0);
+            srow[int64_t(tq) * sstride + int64_t(j) * kRows + tB] = fmaf(sB, vB * fq0, zB * qs0);
+          }
+          if (NU == 2 && tq + 4 < G) {
+            const float vA = float(accU[NU - 1][0]) + 256.f * float(accU[NU - 1][1]) + 65536.f * float(accS[1]);
+            const float vB = float(accU[NU - 1][2]) + 256.f * float(accU[NU - 1][3]) + 65536.f * float(accS[3]);
+            srow[int64_t(tq + 4) * sstride + int64_t(j) * kRows + tA] = fmaf(sA, vA * fq1, zA * qs1);
+            srow[int64_t(tq + 4) * sstride + int64_t(j) * kRows + tB] = fmaf(sB, vB * fq1, zB * qs1);
+          }
+        }
+      } else {
+        // scalar path (rare): lane computes tokens lane and lane+32 for every head
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          const int tt = lane + 32 * half, rg = tt >> 4, t16 = tt & 15;
+          float acc[8];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) acc[g] = 0.f;
+#pragma unroll 1
+          for (int pos = 0; pos < 128; ++pos) {
+            const uint32_t d = desc[rg * 128 + pos];
+            const uint32_t wd = (d >> 18) & 15u;
+            const float code = float(pack_min(blk, rg * 128 + pos) + field_bytes(blk, (d & 0x3ffffu) + t16 * wd, wd));
+            const int c = kpos_to_col(pos, kD);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) acc[g] = fmaf(code, sq[g * kD + c], acc[g]);
+          }
+          const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * tt);
+          const float s = h2f(pr & 0xffff), z = h2f(pr >> 16);
+          for (int g = 0; g < G; ++g) srow[int64_t(g) * sstride + int64_t(j) * kRows + tt] = fmaf(s, acc[g], z * sqsum[g]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty[tk]);
+    }
+    ticket_base += it.nb;
+    if (it.s == 0) {  // uncompressed residue of this unit
+      const int nr = L.nres[it.b];
+      const uint16_t* kr = L.stage + (int64_t(0) * U + it.u) * L.buffer * kD;
+      for (int t = warp; t < nr; t += kCW) {
+        for (int g = 0; g < G; ++g) {
+          float a = 0.f;
+          for (int c = lane; c < kD; c += 32) a = fmaf(__half2float(__ushort_as_half(kr[t * kD + c])), sq[g * kD + c], a);
+          a = warp_sum(a);
+          if (lane == 0) srow[int64_t(g) * sstride + int64_t(it.nbk) * kRows + t] = a;
+        }
       }
     }
   }
 }
 
-constexpr size_t k_smem_bytes() { return kRingBytes + kCW * 512 * 4 + (8 * kD + 16) * 4; }
-constexpr size_t v_smem_bytes() {
-  const size_t a = kRingBytes + kCW * 512 * 4 + (kCW * 8 * kD + 8 + 8 + kCW * 8 + kCW + kCW * 8) * 4;
-  const size_t r = size_t(kCW) * 8 * kD * 4;
-  return a > r ? a : r;
+constexpr size_t k_smem_bytes() { return kRingBytes + kCW * 512 * 4 + (8 * kD + 16) * 4 + 8 * 3 * 32 * 4; }
+constexpr size_t v_smem_bytes() { return kRingBytes + kCW * 512 * 4 + (kCW * 8 * kD + kCW * 8 + kCW) * 4; }
+
+template <class K>
+int persistent_grid(K kernel, size_t smem, int nitems) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, smem);
+  return max(1, min(nitems, max(1, per) * nsm));
 }
 
 }  // namespace
@@ -735,28 +808,40 @@ bool pkv_i8_supported(const pkv_layer_t* L, int G, int64_t stride) {
 int pkv_i8_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
                    cudaStream_t s) {
   const size_t smem = k_smem_bytes();
-  dim3 grid(max(1, (nblocks + kBpc - 1) / kBpc), L->batch * L->heads);
+  const int nsplit = max(1, (nblocks + kBpc - 1) / kBpc);
+  const int nitems = nsplit * L->batch * L->heads;
   if (G <= 4) {
     cudaFuncSetAttribute(fused_k_i8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    fused_k_i8_kernel<1><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, kBpc);
+    const int grid = persistent_grid(fused_k_i8_kernel<1>, smem, nitems);
+    fused_k_i8_kernel<1><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, nsplit, nitems);
   } else {
     cudaFuncSetAttribute(fused_k_i8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    fused_k_i8_kernel<2><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, kBpc);
+    const int grid = persistent_grid(fused_k_i8_kernel<2>, smem, nitems);
+    fused_k_i8_kernel<2><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, nsplit, nitems);
   }
   return pkv_cuda_status(cudaGetLastError(), "pkv_fused_k_scores(i8)");
+}
+
+int64_t pkv_i8_v_scratch(const pkv_layer_t* L, int nblocks, int G) {
+  const int nsplit = max(1, (nblocks + kBpc - 1) / kBpc);
+  const int64_t items = int64_t(nsplit) * L->batch * L->heads;
+  return items * G * (kD + 1) * 4 + int64_t(148 * 8) * kCW * 8 * kD * 4;
 }
 
 int pkv_i8_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
                    float* part, cudaStream_t s) {
   const int nsplit = max(1, (nblocks + kBpc - 1) / kBpc);
-  dim3 grid(nsplit, L->batch * L->heads);
+  const int nitems = nsplit * L->batch * L->heads;
   const size_t smem = v_smem_bytes();
+  float* vscr = part + int64_t(nitems) * G * (kD + 1);
   if (G <= 4) {
     cudaFuncSetAttribute(fused_v_i8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    fused_v_i8_kernel<1><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, kBpc, nsplit);
+    const int grid = min(persistent_grid(fused_v_i8_kernel<1>, smem, nitems), 148 * 8);
+    fused_v_i8_kernel<1><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, nsplit, nitems, vscr);
   } else {
     cudaFuncSetAttribute(fused_v_i8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    fused_v_i8_kernel<2><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, kBpc, nsplit);
+    const int grid = min(persistent_grid(fused_v_i8_kernel<2>, smem, nitems), 148 * 8);
+    fused_v_i8_kernel<2><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, nsplit, nitems, vscr);
   }
   const int64_t total = int64_t(L->batch) * L->heads * G * kD;
   const int fgrid = int((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);

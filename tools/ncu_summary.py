@@ -20,7 +20,11 @@ for k in sys.argv[3:]:
     h = rows[1]; ii = h.index("Instructions Executed"); isrc = h.index("Source")
     st = h.index("Warp Stall Sampling (All Samples)")
     c = Counter(); s = Counter(); tot = 0; stot = 0
+    seen = set()
     for r in rows[2:]:
+        if r and r[0] in seen:  # the source page lists each SASS row twice
+            continue
+        if r: seen.add(r[0])
         if len(r) <= ii: continue
         try: n = int(r[ii])
         except ValueError: continue
