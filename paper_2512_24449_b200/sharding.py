@@ -1,0 +1,125 @@
+"""(batch, kv-head) sharding of the compressed KV cache across GPUs.
+
+The reference has no multi-GPU code (SPEC.md:8 reduces it to a concurrency
+contract; PAPER.md:888-890 runs independent instances).  Following BASELINE.json
+north_star (3): every rank owns a disjoint set of (sequence, kv-head) units —
+its own arena, block tables and staging — so appends and the fused K/V GEMVs
+never cross devices; the only collective is one all-gather of the per-head
+attention outputs per decode step (NCCL over NVLink with the "nccl" backend,
+gloo on CPU in tests).
+
+Partition rule (``plan_partition``): split kv-heads when H % N == 0 (GQA query
+groups stay with their kv-head), else split the batch when B % N == 0; ragged
+splits are not supported (every rank must run the same kernels on the same
+shapes so the all-gather is a single fixed-size collective).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import errors as E
+
+
+@dataclass(frozen=True)
+class Partition:
+    mode: str            # "head" or "batch"
+    world: int
+    rank: int
+    batch: int           # global
+    kv_heads: int        # global
+    b0: int
+    b1: int
+    h0: int
+    h1: int
+
+    @property
+    def local_batch(self) -> int:
+        return self.b1 - self.b0
+
+    @property
+    def local_heads(self) -> int:
+        return self.h1 - self.h0
+
+    def units(self):
+        """Global (b, h) units owned by this rank, b-major."""
+        return [(b, h) for b in range(self.b0, self.b1) for h in range(self.h0, self.h1)]
+
+
+def plan_partition(batch: int, kv_heads: int, world: int, rank: int, prefer: Optional[str] = None) -> Partition:
+    if world <= 0 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    modes = [prefer] if prefer else ["head", "batch"]
+    for mode in modes:
+        if mode == "head" and kv_heads % world == 0:
+            n = kv_heads // world
+            return Partition("head", world, rank, batch, kv_heads, 0, batch, rank * n, (rank + 1) * n)
+        if mode == "batch" and batch % world == 0:
+            n = batch // world
+            return Partition("batch", world, rank, batch, kv_heads, rank * n, (rank + 1) * n, 0, kv_heads)
+    raise E.ShapeMismatchError(f"cannot shard batch={batch} x kv_heads={kv_heads} evenly over {world} ranks")
+
+
+def local_slice(p: Partition, x: torch.Tensor, head_axis: int, batch_axis: int = 0, group: int = 1) -> torch.Tensor:
+    """This rank's slice of a global [B, ..., H*group, ...] tensor."""
+    x = x.narrow(batch_axis, p.b0, p.local_batch)
+    return x.narrow(head_axis, p.h0 * group, p.local_heads * group)
+
+
+def assemble(p: Partition, gathered: torch.Tensor) -> torch.Tensor:
+    """[world, B_loc, Hq_loc, D] all-gathered shards -> global [B, Hq, D]."""
+    if p.mode == "batch":
+        return gathered.reshape(p.world * gathered.shape[1], *gathered.shape[2:])
+    # head split: [world, B, Hq_loc, D] -> [B, world * Hq_loc, D]
+    return gathered.permute(1, 0, 2, 3).reshape(gathered.shape[1], -1, gathered.shape[3])
+
+
+class ShardedDecoder:
+    """One decode step over a sharded cache: local fused K -> softmax -> fused V
+    on this rank's units, then one all-gather of the per-head outputs.
+
+    ``local_attention(q_local) -> out_local`` defaults to the CUDA path
+    (attention_sim.attention_decode_batched on this rank's CompressedStore);
+    tests inject other callables to exercise the partition/collective logic."""
+
+    def __init__(self, partition: Partition, local_attention: Callable[[torch.Tensor], torch.Tensor],
+                 q_heads: int, head_dim: int, group=None):
+        if q_heads % partition.kv_heads:
+            raise E.ShapeMismatchError("q_heads must be a multiple of kv_heads")
+        self.p = partition
+        self.G = q_heads // partition.kv_heads
+        self.q_heads, self.head_dim = q_heads, head_dim
+        self.local_attention = local_attention
+        self.group = group
+        self._gather = None
+
+    def local_q(self, q: torch.Tensor) -> torch.Tensor:
+        """Global q [B, Hq, D] -> this rank's [B_loc, Hq_loc, D]."""
+        return local_slice(self.p, q, head_axis=1, group=self.G).contiguous()
+
+    def step(self, q_local: torch.Tensor) -> torch.Tensor:
+        out_local = self.local_attention(q_local).contiguous()
+        if self.p.world == 1:
+            return out_local
+        shape = (self.p.world,) + tuple(out_local.shape)
+        if self._gather is None or self._gather.shape != shape or self._gather.device != out_local.device:
+            self._gather = torch.empty(shape, dtype=out_local.dtype, device=out_local.device)
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(self._gather.view(-1, *out_local.shape[1:]), out_local, group=self.group)
+        else:
+            dist.all_gather(list(self._gather.unbind(0)), out_local, group=self.group)
+        return assemble(self.p, self._gather)
+
+
+def make_local_store(p: Partition, layers: int, head_dim: int, **kw):
+    """CompressedStore holding this rank's units (CUDA)."""
+    from .kv_store import CompressedStore
+    return CompressedStore(layers, p.local_heads, head_dim, batch=p.local_batch, **kw)
+
+
+def cuda_local_attention(store, layer: int = 0):
+    from .attention_sim import attention_decode_batched
+    return lambda q_local: attention_decode_batched(store, layer, q_local)
