@@ -23,13 +23,13 @@
 
 using namespace pkv;
 
-// int8 tensor-core path for the default format (fused_i8.cu)
-bool pkv_i8_supported(const pkv_layer_t* L, int G, int64_t stride);
-int pkv_i8_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
-                   cudaStream_t s);
-int pkv_i8_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
-                   float* part, cudaStream_t s);
-int64_t pkv_i8_v_scratch(const pkv_layer_t* L, int nblocks, int G);
+// int8 tensor-core path for the default format (fused_fast.cu)
+bool pkv_fast_supported(const pkv_layer_t* L, int G, int64_t stride);
+int pkv_fast_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
+                     cudaStream_t s);
+int pkv_fast_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
+                     float* part, cudaStream_t s);
+int64_t pkv_fast_v_scratch(const pkv_layer_t* L, int nblocks, int G);
 
 namespace {
 
@@ -369,8 +369,8 @@ extern "C" int pkv_fused_k_scores(const pkv_layer_t* L, int32_t nblocks, const f
     return PKV_E_SHAPE;
   }
   cudaStream_t strm = (cudaStream_t)stream;
-  if (pkv_i8_supported(L, G, score_stride) && (reinterpret_cast<uintptr_t>(q) & 15) == 0)
-    return pkv_i8_fused_k(L, nblocks, q, G, scores, score_stride, strm);
+  if (pkv_fast_supported(L, G, score_stride) && (reinterpret_cast<uintptr_t>(q) & 15) == 0)
+    return pkv_fast_fused_k(L, nblocks, q, G, scores, score_stride, strm);
   PKV_DISPATCH_KD(L->pack_size, L->head_dim, return (launch_k<KPc, Dc>(L, nblocks, q, G, scores, score_stride, strm)));
   return PKV_OK;
 }
@@ -380,7 +380,7 @@ extern "C" int64_t pkv_fused_v_scratch_bytes(const pkv_layer_t* L, int32_t nbloc
   if (fused_args(L, nblocks, q_heads, &G)) return -1;
   const int nsplit = max(1, (nblocks + kBpc - 1) / kBpc);
   const int64_t v1 = int64_t(L->batch) * L->heads * nsplit * G * (L->head_dim + 1) * 4;
-  const int64_t i8 = pkv_i8_supported(L, G, 4) ? pkv_i8_v_scratch(L, nblocks, G) : 0;
+  const int64_t i8 = pkv_fast_supported(L, G, 4) ? pkv_fast_v_scratch(L, nblocks, G) : 0;
   return v1 > i8 ? v1 : i8;
 }
 
@@ -396,8 +396,8 @@ extern "C" int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const f
   }
   cudaStream_t strm = (cudaStream_t)stream;
   float* part = (float*)scratch;
-  if (pkv_i8_supported(L, G, w_stride) && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
-    return pkv_i8_fused_v(L, nblocks, w, G, w_stride, out, part, strm);
+  if (pkv_fast_supported(L, G, w_stride) && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
+    return pkv_fast_fused_v(L, nblocks, w, G, w_stride, out, part, strm);
   if (G <= 4) {
     PKV_DISPATCH_KD(L->pack_size, L->head_dim,
                     return (launch_v<KPc, Dc, 4>(L, nblocks, w, G, w_stride, out, part, strm)));

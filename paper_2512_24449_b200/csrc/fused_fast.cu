@@ -1,0 +1,973 @@
+// fused_fast.cu — fused decompress + GEMV for the default format (pack size 16,
+// head_dim 128, 64-token blocks), sm_100a.
+//
+// Persistent CTAs: 4 consumer warps + 1 producer warp.  A work item is one
+// (sequence, kv-head) unit and a run of <= 32 of its blocks; CTA c owns items
+// c, c + gridDim.x, ...
+//  * Producer: one lane streams every block of the CTA's items with 1-D TMA
+//    bulk copies (cp.async.bulk + mbarrier complete_tx) into a byte ring; a
+//    global ticket sequence keeps the ring full across item boundaries.  It
+//    waits for free space with a suspending try_wait (no spinning: a spinning
+//    producer steals issue slots from the consumers on its SM sub-partition).
+//  * Consumer warp w owns blocks w, w+4, ... of the item.  Lane l walks a run
+//    of physically consecutive packs (SPEC.md:330 payloads are contiguous in
+//    physical pack order), so one warp prefix scan of the width nibbles
+//     gives each lane its starting bit and the lane then advances
+//    by 16*w bits per pack — no per-pack descriptor table.
+//  * Unpack (pack size 16, width w <= 4): two funnel shifts extract the pack's
+//    64-bit payload, a 16-entry shared-memory table gives the width's shift
+//    multipliers and byte mask, and a three-level select tree places the 16
+//    fields into 4 registers of 4 bytes with the pack minimum added, i.e. the
+//    exact uint8 codes (SPEC.md:120 q values).  Byte order within a pack:
+//    position m holds row tok(m) = m with bits 1 and 2 swapped.
+//  * Products on the int8 tensor cores (mma.sync m16n8k32, IMMA).  The other
+//    operand is exact fixed point: the query (K) in 3 byte digits (~23 bits),
+//    w_t*scale_t (V, non-negative) in 2 unsigned byte digits scaled per block
+//    and head, so every tile sum is exact in int32.
+//  * K: the reduction runs over channels but packs run along
+//    rows, so every lane stores its decoded packs (16 rows of one channel =
+//    16 bytes) into a per-warp [row-group][channel][16] tile and
+//    ldmatrix.m16n16.trans.b8 reads them back transposed as the A fragment.
+//    score = s_t * (acc / 2^S) + z_t * sum(q)  (dequantisation factored).
+//  * V: rows are the MMA k dimension, the pack direction, so
+//    the decoded registers are the A fragment directly (no transpose).
+//    out = sum_t (w_t s_t) code + sum_t w_t z_t.
+// Blocks with a pack wider than 4 bits or a large minimum take a scalar path
+// inside the same launch (never at the default rel 0.1 / 0.2).
+#include "pkv_common.cuh"
+
+using namespace pkv;
+
+namespace {
+
+constexpr int kRows = 64, kD = 128, kP = 16;
+constexpr int kNib = 8, kMin = 8 + 256, kPar = kMin + 1024, kHdr = kPar + 256;  // 1544
+constexpr int kRing = 20 * 1024;
+constexpr int kTickets = 8;
+constexpr int kCW = 4;
+constexpr int kThreads = (kCW + 1) * 32;
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// try_wait with a suspend-time hint: the thread sleeps until the phase
+// completes (or the hint expires) instead of spinning on the issue port.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32) : "memory");
+}
+// A fragment of m16n8k32 (rows = bytes of 16-byte smem rows, k = smem rows),
+// i.e. a byte transpose of 32 smem rows; lane L gives the address of row L.
+__device__ __forceinline__ void ldsm_t(uint32_t (&a)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m16n16.x2.trans.shared.b8 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"(addr));
+}
+// D = A(u8 16x32) * B(u8 32x8) + C
+__device__ __forceinline__ void imma_uu(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// D = A(u8) * B(s8) + C
+__device__ __forceinline__ void imma_us(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float h2f(uint32_t bits16) { return __half2float(__ushort_as_half(uint16_t(bits16))); }
+
+// a*b + c forced onto the FMA pipe (IMAD); the ALU pipe carries the selects.
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t umulhi(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_t s) {
+  uint32_t d;
+  asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
+  return d;
+}
+__device__ __forceinline__ uint32_t shf_r_clamp(uint32_t lo, uint32_t hi, uint32_t s) {
+  uint32_t d;
+  asm("shf.r.clamp.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
+  return d;
+}
+
+// ---------------------------------------------------------------- unpack
+// Per-width constants (w <= 4): MA = 2^(16-4w), MB = 2^(32-2w), MC = 2^(8-w),
+// byte mask (2^w - 1) * 0x01010101.  Entry w at lut + 16*w.
+__device__ __forceinline__ void init_lut(uint4* lut, int tid) {
+  if (tid < 16) {
+    const uint32_t w = tid <= 4 ? tid : 4;
+    lut[tid] = make_uint4(1u << (16 - 4 * w), w ? 1u << (32 - 2 * w) : 0u, 1u << (8 - w),
+                          ((1u << w) - 1u) * 0x01010101u);
+  }
+}
+
+// (mask & a) | (~mask & b) in one LOP3 with the mask as its immediate
+template <uint32_t M>
+__device__ __forceinline__ uint32_t sel(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "n"(M), "r"(a), "r"(b));
+  return d;
+}
+
+// 8 fields of width w at stride w in x -> two registers of 4 bytes (fields
+// 0,1,4,5 and 2,3,6,7), masked to w bits, plus mr = min * 0x01010101.
+// Shifts are multiplies (FMA pipe), selects and masks are LOP3 (ALU pipe).
+__device__ __forceinline__ void spread8(uint32_t x, const uint4& c, uint32_t mr, uint32_t& ra, uint32_t& rb) {
+  const uint32_t t = sel<0x0000ffffu>(x, imad(x, c.x, 0u));  // fields 4..7 -> bit 16
+  const uint32_t tb = umulhi(t, c.y);                          // t >> 2w
+  const uint32_t ua = sel<0x00ff00ffu>(t, imad(t, c.z, 0u));
+  const uint32_t ub = sel<0x00ff00ffu>(tb, imad(tb, c.z, 0u));
+  ra = imad(ua & c.w, 1u, mr);
+  rb = imad(ub & c.w, 1u, mr);
+}
+
+// Shared-memory operands of one pack: the 3 words covering its <= 64-bit
+// payload (payload starts at bit `bit` of the block, bit % 16 == 0) and the
+// width's table entry.  Issued one pack ahead of the arithmetic.
+struct PackLd {
+  uint32_t w0, w1, w2;
+  uint4 c;
+};
+__device__ __forceinline__ PackLd pack_load(const uint8_t* __restrict__ blk, const uint8_t* __restrict__ lutb,
+                                            uint32_t bit, uint32_t w16) {
+  const uint32_t* p = (const uint32_t*)blk + (bit >> 5);
+  PackLd r;
+  r.w0 = p[0];
+  r.w1 = p[1];
+  r.w2 = p[2];
+  r.c = *(const uint4*)(lutb + w16);
+  return r;
+}
+// r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
+__device__ __forceinline__ void pack_decode(const PackLd& L, uint32_t bit, uint32_t mr, uint32_t (&r)[4]) {
+  const uint32_t x0 = shf_r_wrap(L.w0, L.w1, bit);  // payload bits 0..31
+  const uint32_t x1 = shf_r_wrap(L.w1, L.w2, bit);  // payload bits 32..63
+  const uint32_t md = imad(L.c.x, L.c.x, 0u);       // 2^(32-8w)
+  const uint32_t xh = imad(x1, md, umulhi(x0, md));  // fields 8..15 = payload >> 8w
+  spread8(x0, L.c, mr, r[0], r[1]);
+  spread8(xh, L.c, mr, r[2], r[3]);
+}
+// width of pack i of a lane's 16 (nibbles nb), times 16
+__device__ __forceinline__ uint32_t w16_of(const uint2& nb, int i) {
+  const uint32_t nw = i < 8 ? nb.x : nb.y;
+  const int sh = 4 * (i & 7);
+  return (sh >= 4 ? (nw >> (sh - 4)) : (nw << 4)) & 0xf0u;
+}
+__device__ __forceinline__ uint32_t min_rep(const uint32_t (&mn)[8], int i) {
+  return __byte_perm(mn[i >> 1], 0u, (i & 1) ? 0x2222u : 0x0000u);
+}
+// byte position m within a pack's 16 bytes -> row within the row-group
+__host__ __device__ __forceinline__ int tok(int m) { return (m & 9) | ((m & 2) << 1) | ((m & 4) >> 1); }
+
+// Generic scalar field read (any width <= 15) for the slow path.
+__device__ __forceinline__ uint32_t field_at(const uint8_t* __restrict__ blk, uint32_t bitpos, uint32_t w) {
+  if (w == 0) return 0;
+  const uint8_t* p = blk + (bitpos >> 3);
+  const uint32_t sh = bitpos & 7;
+  const uint32_t v = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16);
+  return (v >> sh) & ((1u << w) - 1u);
+}
+__device__ __forceinline__ uint32_t pack_min(const uint8_t* __restrict__ blk, int p) {
+  return uint32_t(blk[kMin + 2 * p]) | (uint32_t(blk[kMin + 2 * p + 1]) << 8);
+}
+
+// ---------------------------------------------------------------- block parse
+// Lane `chunk` reads the width nibbles of physical packs 16*chunk .. +15 and its
+// 16 minima.  Returns the lane's starting payload bit (warp scan over chunks in
+// lane order) and whether every pack of the block fits the fast path
+// (w <= 4 and minimum <= 240, so min + 15 fits a byte).
+struct Chunk {
+  uint2 nb;       // 16 width nibbles
+  uint32_t mn[8]; // 16 u16 minima
+  uint32_t bit;   // payload bit offset of the chunk's first pack
+};
+__device__ __forceinline__ bool parse_chunk(const uint8_t* __restrict__ blk, int lane, Chunk& ch) {
+  ch.nb = *(const uint2*)(blk + kNib + 8 * lane);
+  const uint2* mp = (const uint2*)(blk + kMin + 32 * lane);
+  uint32_t mor = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint2 v = mp[q];
+    ch.mn[2 * q] = v.x;
+    ch.mn[2 * q + 1] = v.y;
+    mor |= v.x | v.y;
+  }
+  const uint32_t nx = ch.nb.x, ny = ch.nb.y;
+  const uint32_t bad = ((nx | ny) & 0x88888888u) |
+                       (((nx >> 2) & (nx | (nx >> 1))) & 0x11111111u) | (((ny >> 2) & (ny | (ny >> 1))) & 0x11111111u);
+  const bool ok = bad == 0 && ((mor | (mor >> 16)) & 0xffffu) <= 240u;
+  uint32_t a = (nx & 0x0f0f0f0fu) + ((nx >> 4) & 0x0f0f0f0fu) + (ny & 0x0f0f0f0fu) + ((ny >> 4) & 0x0f0f0f0fu);
+  a = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu);
+  const uint32_t lsum = 16u * ((a & 0xffffu) + (a >> 16));  // payload bits (k = 16)
+  uint32_t inc = lsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(PKV_FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  ch.bit = 8u * kHdr + inc - lsum;
+  return __all_sync(PKV_FULL, ok);
+}
+
+// Slow-path descriptor table for any widths: desc[p] = payload bit (from the
+// block start, 18 bits) | width << 18.  Lane l covers packs 16l..16l+15.
+__device__ __forceinline__ void build_desc(const Chunk& ch, int lane, uint32_t* __restrict__ desc) {
+  uint32_t bit = ch.bit;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t w = ((i < 8 ? ch.nb.x : ch.nb.y) >> (4 * (i & 7))) & 15u;
+    desc[16 * lane + i] = bit | (w << 18);
+    bit += 16u * w;
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- work split
+// The layer's blocks are numbered gb = u * NB + j (unit u = b * H + h, block j,
+// NB = blocks per sequence; sequences advance in lockstep).  CTA c of a grid of
+// N owns the contiguous range [T*c/N, T*(c+1)/N) of the T = U*NB blocks, so
+// every CTA gets the same work to within one block (no tail of idle SMs), and
+// a range spans only a few units.  Ticket t of a CTA is block b0 + t; consumer
+// warp w takes tickets w, w + kCW, ...
+struct Range {
+  int64_t b0, b1;
+};
+__device__ __forceinline__ Range cta_range(int64_t total) {
+  Range r;
+  r.b0 = total * blockIdx.x / gridDim.x;
+  r.b1 = total * (blockIdx.x + 1) / gridDim.x;
+  return r;
+}
+__host__ __device__ __forceinline__ int64_t cta_of(int64_t gb, int64_t total, int grid) {
+  return ((gb + 1) * grid - 1) / total;
+}
+
+// ---------------------------------------------------------------- ring
+struct Ring {
+  uint8_t* data;
+  uint64_t* full;
+  uint64_t* empty;
+  uint32_t* start;  // [kTickets] ring offset of each ticket's block
+  uint32_t* abs;    // [kTickets] producer-private absolute start
+  int64_t* soff;    // [32] producer-private block offsets (staged table)
+  int* slen;        // [32] byte length, -1 = no block (past nblk)
+};
+constexpr size_t kRingBytes = kRing + kTickets * 16 + kTickets * 8 + 32 * 12;
+
+__device__ __forceinline__ uint8_t* setup_ring(uint8_t* smem, Ring& R) {
+  R.data = smem;
+  R.full = (uint64_t*)(smem + kRing);
+  R.empty = R.full + kTickets;
+  R.start = (uint32_t*)(R.empty + kTickets);
+  R.abs = R.start + kTickets;
+  R.soff = (int64_t*)(R.abs + kTickets);
+  R.slen = (int*)(R.soff + 32);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTickets; ++s) {
+      mbar_init(&R.full[s], 1);
+      mbar_init(&R.empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  return smem + kRingBytes;
+}
+
+// Producer warp: stages 32 directory entries at a time (lane-parallel), then
+// lane 0 issues one TMA bulk copy per block into the ring (tickets in block
+// order).  A block past its sequence's nblk gets a plain arrive (no copy).
+__device__ void produce(const Ring& R, const pkv_layer_t& L, int kind, int NB, Range rg, int lane) {
+  const int U = L.batch * L.heads;
+  uint32_t head = 0;
+  int oldest = 0, ticket = 0;
+  for (int64_t g0 = rg.b0; g0 < rg.b1; g0 += 32) {
+    const int n = int((rg.b1 - g0 < 32 ? rg.b1 - g0 : 32));
+    if (lane < n) {
+      const int64_t gb = g0 + lane;
+      const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
+      const int64_t tab = (int64_t(kind) * U + u) * L.max_blocks + j;
+      const bool ok = j < L.nblk[u / L.heads];
+      R.soff[lane] = ok ? L.blk_off[tab] : 0;
+      R.slen[lane] = ok ? L.blk_len[tab] : -1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i, ++ticket) {
+        const int tk = ticket % kTickets;
+        const int len = R.slen[i];
+        const uint32_t bytes = len < 0 ? 0u : uint32_t((len + 15) & ~15);
+        const uint32_t size = len < 0 ? 0u : bytes + 16;  // +16: slack for the decoders' word over-reads
+        uint32_t pos = head % kRing;
+        if (pos + size > kRing) {
+          head += kRing - pos;
+          pos = 0;
+        }
+        while (oldest < ticket &&
+               ((ticket - oldest) >= kTickets || head + size - R.abs[oldest % kTickets] > kRing)) {
+          mbar_wait(&R.empty[oldest % kTickets], uint32_t((oldest / kTickets) & 1));
+          ++oldest;
+        }
+        R.abs[tk] = head;
+        R.start[tk] = pos;
+        if (len < 0) {
+          mbar_arrive(&R.full[tk]);
+        } else {
+          mbar_expect_tx(&R.full[tk], bytes);
+          tma_load_1d(R.data + pos, L.arena + R.soff[i], bytes, &R.full[tk]);
+        }
+        head += size;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ======================================================================= K
+// Per-warp tile: [row-group g][channel c][16 bytes], row R = 128g + c at byte
+// 16 * (R ^ (((R >> 6) & 1) << 2)) (XOR swizzle of the 16-byte chunk within a
+// 128-byte line: each quarter-warp of a decode step's STS.128 and each 8-row
+// phase of the ldmatrix hit 8 distinct chunks, i.e. no bank conflicts).
+constexpr int kTile = 4 * 128 * 16;  // 8 KB
+
+__device__ __forceinline__ float sel8(const float (&v)[8], int i) {
+  float r = v[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) r = i == k ? v[k] : r;
+  return r;
+}
+
+// Query operand of one unit for this lane (B fragments of the IMMA): k-step jj
+// covers channels 32jj..32jj+31, b0 = channels 32jj + 4tq + e, b1 = +16.
+// Column gi of unsigned tile nu = (head 4nu + gi/2, byte digit gi&1) of
+// x = rint(q * f_head) (|x| <= 2^22, f_head a power of two); signed tile S
+// column 2t = (head t, digit 2), 2t+1 = (head t+4, digit 2) or zero.
+template <int NU>
+struct QFrag {
+  uint32_t u[NU][4][2], s[4][2];
+  float qs[2], inv[2];  // sum(q) and 1/f of heads tq and tq+4
+};
+template <int NU>
+__device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G, int lane, QFrag<NU>& F) {
+  const int gi = lane >> 2, tq = lane & 3;
+  float mx[8], sm[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g < G) v = *(const float4*)(qu + g * kD + 4 * lane);
+    mx[g] = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+    sm[g] = (v.x + v.y) + (v.z + v.w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      mx[g] = fmaxf(mx[g], __shfl_xor_sync(PKV_FULL, mx[g], o));
+      sm[g] += __shfl_xor_sync(PKV_FULL, sm[g], o);
+    }
+  float f[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const int eb = (__float_as_int(mx[g]) >> 23) & 0xff;
+    // f = 2^(21 - e) for max in [2^e, 2^(e+1)): |q * f| < 2^22
+    f[g] = __int_as_float(max(1, min(275 - eb, 254)) << 23);
+  }
+  F.qs[0] = sel8(sm, tq);
+  F.qs[1] = sel8(sm, tq + 4);
+  F.inv[0] = 1.f / sel8(f, tq);
+  F.inv[1] = 1.f / sel8(f, tq + 4);
+  // x = rint(q*f) via the 1.5*2^23 magic: bits - 0x4B400000 = x for |x| < 2^22;
+// digits: byte 0, byte 1 (unsigned) and byte 2 (signed: x >> 16)
+  auto digits = [&](int g, int jj, int r, uint32_t (&x)[4]) {
+    const float4 v = *(const float4*)(qu + g * kD + 32 * jj + 16 * r + 4 * tq);
+    const float fg = sel8(f, g);
+    x[0] = __float_as_uint(fmaf(v.x, fg, 12582912.f)) - 0x4B400000u;
+    x[1] = __float_as_uint(fmaf(v.y, fg, 12582912.f)) - 0x4B400000u;
+    x[2] = __float_as_uint(fmaf(v.z, fg, 12582912.f)) - 0x4B400000u;
+    x[3] = __float_as_uint(fmaf(v.w, fg, 12582912.f)) - 0x4B400000u;
+  };
+  const int gsS = (gi >> 1) + 4 * (gi & 1);
+  const bool useS = ((gi & 1) == 0 || NU == 2) && gsS < G;
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int nu = 0; nu < NU; ++nu) {
+        const int g = 4 * nu + (gi >> 1);
+        uint32_t x[4] = {0u, 0u, 0u, 0u};
+        if (g < G) digits(g, jj, r, x);
+        const uint32_t lo = __byte_perm(x[0], x[1], (gi & 1) ? 0x0051u : 0x0040u);
+        const uint32_t hi = __byte_perm(x[2], x[3], (gi & 1) ? 0x0051u : 0x0040u);
+        F.u[nu][jj][r] = __byte_perm(lo, hi, 0x5410u);
+      }
+      uint32_t x[4] = {0u, 0u, 0u, 0u};
+      if (useS) digits(gsS, jj, r, x);
+      const uint32_t lo = __byte_perm(x[0], x[1], 0x0062u);
+      const uint32_t hi = __byte_perm(x[2], x[3], 0x0062u);
+      F.s[jj][r] = __byte_perm(lo, hi, 0x5410u);
+    }
+}
+
+template <int NU>  // unsigned query digit tiles: 1 for G <= 4, 2 for G <= 8
+__global__ void __launch_bounds__(kThreads, 4) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
+                                                                    float* __restrict__ scores, int64_t sstride, int NB,
+                                                                    int64_t total) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring R;
+  uint8_t* rest = setup_ring(smem, R);
+  uint8_t* tiles = rest;                       // [kCW][kTile]
+  uint4* lut = (uint4*)(tiles + kCW * kTile);  // [16]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gi = lane >> 2, tq = lane & 3;
+  const int U = L.batch * L.heads, Hq = L.heads * G;
+  const Range rg = cta_range(total);
+  init_lut(lut, threadIdx.x);
+  __syncthreads();
+  if (warp == kCW) {  // producer; no CTA-wide barrier follows
+    produce(R, L, 0, NB, rg, lane);
+    return;
+  }
+  uint8_t* tile = tiles + warp * kTile;
+  const uint32_t tile_s = smem_u32(tile);
+  const uint8_t* lutb = (const uint8_t*)lut;
+  // STS offsets: lane l's pack i (physical 16l + i) is row-group l >> 3,
+  // channel 64(l&1) + 4i + ((l>>1)&3); even/odd i differ in bit 2 of the chunk
+  const uint32_t R0 = 128u * (lane >> 3) + 64u * (lane & 1) + ((lane >> 1) & 3);
+  const uint32_t X = 4u * (lane & 1);
+  const uint32_t st_even = 16u * ((R0 & ~7u) | ((R0 & 7u) ^ X));
+  const uint32_t st_odd = 16u * ((R0 & ~7u) | (((R0 & 7u) | 4u) ^ X));
+  QFrag<NU> F;
+  int cur_u = -1;
+  const int n = int(rg.b1 - rg.b0);
+
+#pragma unroll 1
+  for (int t = warp; t < n; t += kCW) {
+    const int64_t gb = rg.b0 + t;
+    const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
+    const int b = u / L.heads, h = u - b * L.heads;
+    if (u != cur_u) {
+      build_qfrag<NU>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, F);
+      cur_u = u;
+    }
+    float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride + int64_t(j) * kRows;
+    const int tk = t % kTickets;
+    mbar_wait(&R.full[tk], uint32_t((t / kTickets) & 1));
+    if (j >= L.nblk[b]) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty[tk]);
+      continue;
+    }
+    const uint8_t* blk = R.data + R.start[tk];
+    Chunk ch;
+    const bool fast = parse_chunk(blk, lane, ch);
+    if (fast) {
+      uint32_t bit = ch.bit;
+      uint32_t w16 = w16_of(ch.nb, 0);
+      PackLd cur = pack_load(blk, lutb, bit, w16);
+#pragma unroll
+      for (int i2 = 0; i2 < 16; ++i2) {
+        const uint32_t nbit = bit + w16;
+        const uint32_t nw16 = i2 < 15 ? w16_of(ch.nb, i2 + 1) : 0u;
+        PackLd nxt;
+        if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
+        uint32_t r[4];
+        pack_decode(cur, bit, min_rep(ch.mn, i2), r);
+        *(uint4*)(tile + ((i2 & 1) ? st_odd : st_even) + 128u * (i2 >> 1)) = make_uint4(r[0], r[1], r[2], r[3]);
+        bit = nbit;
+        w16 = nw16;
+        if (i2 < 15) cur = nxt;
+      }
+      // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
+      uint32_t prm[4][2];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        prm[g][0] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi)));
+        prm[g][1] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi) + 8));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty[tk]);  // ring slot no longer read
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        int accU[NU][4], accS[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          accS[e] = 0;
+#pragma unroll
+          for (int nu = 0; nu < NU; ++nu) accU[nu][e] = 0;
+        }
+        // lane L addresses row R = 128g + 32jj + L
+        const uint32_t a0 = tile_s + 16u * (128u * g + lane);              // jj = 0, 1 (+512 B)
+        const uint32_t a1 = tile_s + 16u * (128u * g + (lane ^ 4u) + 64u);  // jj = 2, 3
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          uint32_t a[4];
+          ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
+#pragma unroll
+          for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, F.u[nu][jj][0], F.u[nu][jj][1]);
+          imma_us(accS, a, F.s[jj][0], F.s[jj][1]);
+        }
+        const int tA = 16 * g + tok(gi), tB = tA + 8;
+        const float sA = h2f(prm[g][0] & 0xffff), zA = h2f(prm[g][0] >> 16);
+        const float sB = h2f(prm[g][1] & 0xffff), zB = h2f(prm[g][1] >> 16);
+        if (tq < G) {
+          const float vA = float(accU[0][0]) + 256.f * float(accU[0][1]) + 65536.f * float(accS[0]);
+          const float vB = float(accU[0][2]) + 256.f * float(accU[0][3]) + 65536.f * float(accS[2]);
+          srow[int64_t(tq) * sstride + tA] = fmaf(sA, vA * F.inv[0], zA * F.qs[0]);
+          srow[int64_t(tq) * sstride + tB] = fmaf(sB, vB * F.inv[0], zB * F.qs[0]);
+        }
+        if (NU == 2 && tq + 4 < G) {
+          const float vA = float(accU[NU - 1][0]) + 256.f * float(accU[NU - 1][1]) + 65536.f * float(accS[1]);
+          const float vB = float(accU[NU - 1][2]) + 256.f * float(accU[NU - 1][3]) + 65536.f * float(accS[3]);
+          srow[int64_t(tq + 4) * sstride + tA] = fmaf(sA, vA * F.inv[1], zA * F.qs[1]);
+          srow[int64_t(tq + 4) * sstride + tB] = fmaf(sB, vB * F.inv[1], zB * F.qs[1]);
+        }
+      }
+      __syncwarp();  // tile reads done before the next block's stores
+    } else {
+      // scalar path (rare): lane computes rows lane and lane+32 for every head
+      const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
+      uint32_t* desc = (uint32_t*)tile;
+      build_desc(ch, lane, desc);
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int tt = lane + 32 * half, rgp = tt >> 4, t16 = tt & 15;
+        const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * tt);
+        const float s = h2f(pr & 0xffff), z = h2f(pr >> 16);
+#pragma unroll 1
+        for (int g = 0; g < G; ++g) {
+          float acc = 0.f, qsum = 0.f;
+#pragma unroll 1
+          for (int pos = 0; pos < 128; ++pos) {
+            const uint32_t d = desc[rgp * 128 + pos];
+            const uint32_t wd = d >> 18;
+            const float code = float(pack_min(blk, rgp * 128 + pos) + field_at(blk, (d & 0x3ffffu) + t16 * wd, wd));
+            const float qc = qu[g * kD + kpos_to_col(pos, kD)];
+            acc = fmaf(code, qc, acc);
+            qsum += qc;
+          }
+          srow[int64_t(g) * sstride + tt] = fmaf(s, acc, z * qsum);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty[tk]);
+    }
+  }
+  // uncompressed residue rows of units u = blockIdx.x, blockIdx.x + grid, ...
+  for (int u = blockIdx.x; u < U; u += gridDim.x) {
+    const int b = u / L.heads, h = u - b * L.heads;
+    const int nr = L.nres[b];
+    const uint16_t* kr = L.stage + (int64_t(0) * U + u) * L.buffer * kD;
+    const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
+    float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride + int64_t(L.nblk[b]) * kRows;
+    for (int t = warp; t < nr; t += kCW) {
+      for (int g = 0; g < G; ++g) {
+        float a = 0.f;
+        for (int c = lane; c < kD; c += 32) a = fmaf(__half2float(__ushort_as_half(kr[t * kD + c])), qu[g * kD + c], a);
+        a = warp_sum(a);
+        if (lane == 0) srow[int64_t(g) * sstride + t] = a;
+      }
+    }
+  }
+}
+
+// ======================================================================= V
+// Lane (gi, tq) decodes physical packs 128tq + 16gi + i (row-group tq, channel
+// 16gi + i), i = 0..15, two per m-tile: rows gi / gi+8 of m-tile mt are
+// channels 16gi + 2mt / +1.  k-chunk tq <-> row-group tq bytes 0..3 (k-step 0)
+// / 8..11 (k-step 1), chunk tq+4 <-> bytes 4..7 / 12..15.  The B operand
+// (rows x [head, digit]) comes from a per-warp [head][digit][64] byte array
+// in the same byte order.  D columns 2tq, 2tq+1 = head tq digits 0, 1, so lane
+// (gi, tq) owns out[head 4nt + tq][channels 16gi .. 16gi+15].  Per (CTA range
+// segment = unit, warp) partial sums go to scratch; the finalize kernel adds
+// them in a fixed order (deterministic) plus the residue.
+constexpr int kPart = kD + 4;  // 128 channels, the z term, padding (16-byte rows)
+
+template <int NT>  // n-tiles: 1 for G <= 4, 2 for G <= 8
+__global__ void __launch_bounds__(kThreads, 4) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
+                                                                    int64_t wstride, float* __restrict__ part, int NB,
+                                                                    int64_t total, int maxseg,
+                                                                    float* __restrict__ vscr) {
+  constexpr int GP = 4 * NT;    // padded heads
+  constexpr int LPH = 32 / GP;  // writer lanes per head
+  constexpr int TPL = 64 / LPH; // rows per writer lane (8 or 16)
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring R;
+  uint8_t* rest = setup_ring(smem, R);
+  uint32_t* desc_all = (uint32_t*)rest;                  // [kCW][512] (slow path)
+  uint8_t* frag_all = (uint8_t*)(desc_all + kCW * 512);  // [kCW][GP][2][64]
+  uint4* lut = (uint4*)(frag_all + kCW * GP * 128);      // [16]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gi = lane >> 2, tq = lane & 3;
+  const int Hq = L.heads * G;
+  const Range rg = cta_range(total);
+  init_lut(lut, threadIdx.x);
+  __syncthreads();
+  if (warp == kCW) {
+    produce(R, L, 1, NB, rg, lane);
+    return;
+  }
+  uint32_t* desc = desc_all + warp * 512;
+  uint8_t* frag = frag_all + warp * GP * 128;
+  const uint8_t* lutb = (const uint8_t*)lut;
+  float* vsl = vscr + (int64_t(blockIdx.x) * kCW + warp) * (8 * kD);  // scalar-path partials [8][kD]
+  // writer role for the B operand: head wh, rows wt0 .. wt0 + TPL - 1
+  const int wh = lane / LPH, wt0 = (lane % LPH) * TPL;
+  const int n = int(rg.b1 - rg.b0);
+  const int u_first = int(rg.b0 / NB);
+  const int u_last = n > 0 ? int((rg.b1 - 1) / NB) : u_first - 1;
+
+  float acc[NT][16];
+  float zacc = 0.f;
+  bool slow_used = false;
+  int seg = 0;  // segment (unit - u_first) the accumulators belong to
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[nt][i] = 0.f;
+  // write the accumulators of segment `seg` (then zero them)
+  auto flush = [&]() {
+    float* pp = part + ((int64_t(blockIdx.x) * maxseg + seg) * kCW + warp) * G * kPart;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int g = 4 * nt + tq;
+      if (g < G) {
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4)
+          *(float4*)(pp + g * kPart + 16 * gi + 4 * i4) =
+              make_float4(acc[nt][4 * i4], acc[nt][4 * i4 + 1], acc[nt][4 * i4 + 2], acc[nt][4 * i4 + 3]);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[nt][i] = 0.f;
+    }
+    float z = zacc;
+#pragma unroll
+    for (int o = 1; o < LPH; o <<= 1) z += __shfl_xor_sync(PKV_FULL, z, o);
+    if (lane % LPH == 0 && wh < G) pp[wh * kPart + kD] = z;
+    zacc = 0.f;
+    if (slow_used) {
+      __syncwarp();
+      for (int e = lane; e < G * kD; e += 32) {
+        const int g = e / kD, c = e - g * kD;
+        pp[g * kPart + c] += vsl[g * kD + c];
+        vsl[g * kD + c] = 0.f;
+      }
+      slow_used = false;
+    }
+    ++seg;
+  };
+  // weights of this warp's first block (prefetched one block ahead)
+  float wn[TPL];
+  auto load_w = [&](int t) {
+    const int64_t gb = rg.b0 + t;
+    const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
+    const int b = u / L.heads, h = u - b * L.heads;
+    const float* wrow = w + (int64_t(b) * Hq + int64_t(h) * G + wh) * wstride + int64_t(j) * kRows + wt0;
+    const bool ok = t < n && wh < G;
+#pragma unroll
+    for (int q4 = 0; q4 < TPL / 4; ++q4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) v = *(const float4*)(wrow + 4 * q4);
+      wn[4 * q4] = v.x; wn[4 * q4 + 1] = v.y; wn[4 * q4 + 2] = v.z; wn[4 * q4 + 3] = v.w;
+    }
+  };
+  load_w(warp);
+
+#pragma unroll 1
+  for (int t = warp; t < n; t += kCW) {
+    const int64_t gb = rg.b0 + t;
+    const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
+    const int b = u / L.heads, h = u - b * L.heads;
+    while (seg < u - u_first) flush();
+    float wc[TPL];
+#pragma unroll
+    for (int e = 0; e < TPL; ++e) wc[e] = wn[e];
+    load_w(t + kCW);
+    const int tk = t % kTickets;
+    mbar_wait(&R.full[tk], uint32_t((t / kTickets) & 1));
+    if (j >= L.nblk[b]) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty[tk]);
+      continue;
+    }
+    const uint8_t* blk = R.data + R.start[tk];
+    Chunk ch;
+    const bool fast = parse_chunk(blk, lane, ch);
+    // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits, f a power of two
+    // per (block, head) with max x * f < 2^16; z term sum_t w_t z_t in f32
+    float xs[TPL];
+    float mx = 0.f;
+#pragma unroll
+    for (int e2 = 0; e2 < TPL / 2; ++e2) {
+      const uint2 pr = *(const uint2*)(blk + kPar + 4 * (wt0 + 2 * e2));
+      const float s0 = h2f(pr.x & 0xffff), s1 = h2f(pr.y & 0xffff);
+      zacc = fmaf(wc[2 * e2], h2f(pr.x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr.y >> 16), zacc));
+      xs[2 * e2] = wc[2 * e2] * s0;
+      xs[2 * e2 + 1] = wc[2 * e2 + 1] * s1;
+      mx = fmaxf(mx, fmaxf(xs[2 * e2], xs[2 * e2 + 1]));
+    }
+#pragma unroll
+    for (int o = 1; o < LPH; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(PKV_FULL, mx, o));
+    // f = 2^(15 - e) for mx in [2^e, 2^(e+1)): mx * f < 2^16
+    const int eb = (__float_as_int(mx) >> 23) & 0xff;
+    const int fb = min(269 - eb, 254);
+    const float f = __int_as_float(fb << 23);
+    const float invf = __int_as_float((254 - fb) << 23);
+#pragma unroll
+    for (int e8 = 0; e8 < TPL / 8; ++e8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(__fmaf_rz(xs[8 * e8 + e], f, 8388608.f));
+      // byte position p holds row tok(p): (0,1,4,5) then (2,3,6,7)
+      const uint32_t t01 = __byte_perm(v[0], v[1], 0x5140), t45 = __byte_perm(v[4], v[5], 0x5140);
+      const uint32_t t23 = __byte_perm(v[2], v[3], 0x5140), t67 = __byte_perm(v[6], v[7], 0x5140);
+      const uint32_t lo0 = __byte_perm(t01, t45, 0x5410), hi0 = __byte_perm(t01, t45, 0x7632);
+      const uint32_t lo1 = __byte_perm(t23, t67, 0x5410), hi1 = __byte_perm(t23, t67, 0x7632);
+      *(uint2*)(frag + (wh * 2 + 0) * 64 + wt0 + 8 * e8) = make_uint2(lo0, lo1);
+      *(uint2*)(frag + (wh * 2 + 1) * 64 + wt0 + 8 * e8) = make_uint2(hi0, hi1);
+    }
+    __syncwarp();
+    uint32_t bf[NT][4];
+    float inv[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint4 v = *(const uint4*)(frag + ((4 * nt + (gi >> 1)) * 2 + (gi & 1)) * 64 + 16 * tq);
+      bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
+      inv[nt] = __shfl_sync(PKV_FULL, invf, (4 * nt + tq) * LPH);
+    }
+    if (fast) {
+      // lane (gi, tq) = chunk 8tq + gi of the scan
+      const int src = 8 * tq + gi;
+      uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src);
+      const uint2 nb = *(const uint2*)(blk + kNib + 8 * src);
+      uint32_t mn[8];
+      {
+        const uint2* mp = (const uint2*)(blk + kMin + 32 * src);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint2 v = mp[q4];
+          mn[2 * q4] = v.x;
+          mn[2 * q4 + 1] = v.y;
+        }
+      }
+      uint32_t w16 = w16_of(nb, 0);
+      PackLd cur = pack_load(blk, lutb, bit, w16);
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t P[2][4];
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+          const int i2 = 2 * mt + pp;
+          const uint32_t nbit = bit + w16;
+          const uint32_t nw16 = i2 < 15 ? w16_of(nb, i2 + 1) : 0u;
+          PackLd nxt;
+          if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
+          pack_decode(cur, bit, min_rep(mn, i2), P[pp]);
+          bit = nbit;
+          w16 = nw16;
+          if (i2 < 15) cur = nxt;
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          int d[4] = {0, 0, 0, 0};
+          const uint32_t a0[4] = {P[0][0], P[1][0], P[0][1], P[1][1]};
+          imma_uu(d, a0, bf[nt][0], bf[nt][1]);
+          const uint32_t a1[4] = {P[0][2], P[1][2], P[0][3], P[1][3]};
+          imma_uu(d, a1, bf[nt][2], bf[nt][3]);
+          acc[nt][2 * mt] = fmaf(float(d[0] + 256 * d[1]), inv[nt], acc[nt][2 * mt]);
+          acc[nt][2 * mt + 1] = fmaf(float(d[2] + 256 * d[3]), inv[nt], acc[nt][2 * mt + 1]);
+        }
+      }
+    } else {
+      // scalar path (rare): lane owns channels lane + 32q, all 64 rows, all heads;
+      // partials accumulate in this warp's global scratch (fixed order, deterministic)
+      build_desc(ch, lane, desc);
+      if (!slow_used) {
+        for (int e = lane; e < 8 * kD; e += 32) vsl[e] = 0.f;
+        __syncwarp();
+        slow_used = true;
+      }
+      const float* wu = w + (int64_t(b) * Hq + int64_t(h) * G) * wstride + int64_t(j) * kRows;
+      float sacc[8][4];
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) sacc[g][q4] = vsl[g * kD + lane + 32 * q4];
+#pragma unroll 1
+      for (int r = 0; r < kRows; ++r) {
+        const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * r);
+        const float s = h2f(pr & 0xffff);
+        float ws[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) ws[g] = g < G ? wu[int64_t(g) * wstride + r] * s : 0.f;
+        const int rgp = r >> 4, tt = r & 15;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int c = lane + 32 * q4;
+          const uint32_t dd = desc[rgp * 128 + c];
+          const uint32_t wd = dd >> 18;
+          const float code = float(pack_min(blk, rgp * 128 + c) + field_at(blk, (dd & 0x3ffffu) + tt * wd, wd));
+#pragma unroll
+          for (int g = 0; g < 8; ++g) sacc[g][q4] = fmaf(ws[g], code, sacc[g][q4]);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) vsl[g * kD + lane + 32 * q4] = sacc[g][q4];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&R.empty[tk]);
+  }
+  while (seg <= u_last - u_first) flush();
+}
+
+// out[b][h*G+g][c] = sum over the CTAs whose range meets unit u (ascending),
+// their warps (ascending) of part, plus the z terms, plus the residue rows.
+__global__ void fused_v_fast_finalize(pkv_layer_t L, const float* __restrict__ part, const float* __restrict__ w,
+                                      int G, int64_t wstride, int NB, int64_t total, int grid, int maxseg,
+                                      float* __restrict__ out) {
+  const int U = L.batch * L.heads;
+  const int64_t n = int64_t(U) * G * kD;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int(e % kD);
+    const int64_t ug = e / kD;
+    const int g = int(ug % G);
+    const int u = int(ug / G);
+    float s = 0.f, z = 0.f;
+    if (total > 0 && NB > 0) {
+      const int64_t c0 = cta_of(int64_t(u) * NB, total, grid), c1 = cta_of(int64_t(u + 1) * NB - 1, total, grid);
+      for (int64_t cc = c0; cc <= c1; ++cc) {
+        const int seg = u - int((total * cc / grid) / NB);
+        for (int wv = 0; wv < kCW; ++wv) {
+          const float* pp = part + ((cc * maxseg + seg) * kCW + wv) * G * kPart + g * kPart;
+          s += pp[c];
+          z += pp[kD];
+        }
+      }
+    }
+    const int b = u / L.heads;
+    const int nr = L.nres[b];
+    const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
+    const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
+    for (int t = 0; t < nr; ++t) s = fmaf(wr[t], __half2float(__ushort_as_half(vr[t * kD + c])), s);
+    out[e] = s + z;
+  }
+}
+
+constexpr size_t k_smem_bytes() { return kRingBytes + kCW * kTile + 16 * 16; }
+constexpr size_t v_smem_bytes() { return kRingBytes + kCW * 512 * 4 + kCW * 8 * 128 + 16 * 16; }
+
+template <class K>
+int fast_grid(K kernel, size_t smem, int64_t total) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, smem);
+  const int64_t cap = int64_t(max(1, per)) * nsm;
+  return int(total < 1 ? 1 : (total < cap ? total : cap));
+}
+
+int v_grid(const pkv_layer_t* L, int nblocks, int G) {
+  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
+  return G <= 4 ? fast_grid(fused_v_fast_kernel<1>, v_smem_bytes(), total)
+                : fast_grid(fused_v_fast_kernel<2>, v_smem_bytes(), total);
+}
+int v_maxseg(const pkv_layer_t* L, int nblocks, int grid) {
+  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
+  if (nblocks <= 0 || total <= 0) return 1;
+  const int64_t len = (total + grid - 1) / grid;
+  return int((len + nblocks - 1) / nblocks + 1);
+}
+
+}  // namespace
+
+bool pkv_fast_supported(const pkv_layer_t* L, int G, int64_t stride) {
+  return L->pack_size == kP && L->head_dim == kD && L->block == kRows && G >= 1 && G <= 8 && stride % 4 == 0;
+}
+
+int pkv_fast_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
+                     cudaStream_t s) {
+  const size_t smem = k_smem_bytes();
+  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
+  const int U = L->batch * L->heads;
+  const int NB = max(1, nblocks);
+  if (G <= 4) {
+    const int grid = fast_grid(fused_k_fast_kernel<1>, smem, total > U ? total : U);
+    fused_k_fast_kernel<1><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, NB, total);
+  } else {
+    const int grid = fast_grid(fused_k_fast_kernel<2>, smem, total > U ? total : U);
+    fused_k_fast_kernel<2><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, NB, total);
+  }
+  return pkv_cuda_status(cudaGetLastError(), "pkv_fused_k_scores(fast)");
+}
+
+int64_t pkv_fast_v_scratch(const pkv_layer_t* L, int nblocks, int G) {
+  const int grid = v_grid(L, nblocks, G);
+  const int maxseg = v_maxseg(L, nblocks, grid);
+  return (int64_t(grid) * maxseg * kCW * G * kPart + int64_t(grid) * kCW * 8 * kD) * 4;
+}
+
+int pkv_fast_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
+                     float* part, cudaStream_t s) {
+  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
+  const int grid = v_grid(L, nblocks, G);
+  const int maxseg = v_maxseg(L, nblocks, grid);
+  const int NB = max(1, nblocks);
+  float* vscr = part + int64_t(grid) * maxseg * kCW * G * kPart;
+  const size_t smem = v_smem_bytes();
+  if (total > 0) {
+    if (G <= 4)
+      fused_v_fast_kernel<1><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
+    else
+      fused_v_fast_kernel<2><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
+  }
+  const int64_t n = int64_t(L->batch) * L->heads * G * kD;
+  const int fgrid = int((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
+  fused_v_fast_finalize<<<fgrid, 256, 0, s>>>(*L, part, w, G, wstride, NB, total, grid, maxseg, out);
+  return pkv_cuda_status(cudaGetLastError(), "pkv_fused_v_output(fast)");
+}
