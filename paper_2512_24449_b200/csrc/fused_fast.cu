@@ -1,19 +1,17 @@
 // fused_fast.cu — fused decompress + GEMV for the default format (pack size 16,
 // head_dim 128, 64-token blocks), sm_100a.
 //
-// Persistent CTAs: 4 consumer warps + 1 producer warp.  A work item is one
-// (sequence, kv-head) unit and a run of <= 32 of its blocks; CTA c owns items
-// c, c + gridDim.x, ...
-//  * Producer: one lane streams every block of the CTA's items with 1-D TMA
-//    bulk copies (cp.async.bulk + mbarrier complete_tx) into a byte ring; a
-//    global ticket sequence keeps the ring full across item boundaries.  It
-//    waits for free space with a suspending try_wait (no spinning: a spinning
-//    producer steals issue slots from the consumers on its SM sub-partition).
-//  * Consumer warp w owns blocks w, w+4, ... of the item.  Lane l walks a run
-//    of physically consecutive packs (SPEC.md:330 payloads are contiguous in
-//    physical pack order), so one warp prefix scan of the width nibbles
-//     gives each lane its starting bit and the lane then advances
-//    by 16*w bits per pack — no per-pack descriptor table.
+// Warp-level persistent work split: warp W of the grid owns a contiguous,
+// equal-sized range of the layer's (unit, block) sequence, unit = (sequence,
+// kv-head).  Every warp is its own producer:
+//  * it streams its blocks with 1-D TMA bulk copies (cp.async.bulk + mbarrier
+//    complete_tx) into a private shared-memory byte ring, two blocks ahead
+//    (bulk copies issued by one warp are serviced one after another, so a
+//    single producer warp per CTA cannot feed HBM-rate decoding).
+//  * Lane l walks a run of physically consecutive packs (SPEC.md:330 payloads
+//    are contiguous in physical pack order), so one warp prefix scan of the
+//    width nibbles gives each lane its starting bit and the lane
+//    then advances by 16*w bits per pack — no per-pack descriptor table.
 //  * Unpack (pack size 16, width w <= 4): two funnel shifts extract the pack's
 //    64-bit payload, a 16-entry shared-memory table gives the width's shift
 //    multipliers and byte mask, and a three-level select tree places the 16
@@ -42,10 +40,6 @@ namespace {
 
 constexpr int kRows = 64, kD = 128, kP = 16;
 constexpr int kNib = 8, kMin = 8 + 256, kPar = kMin + 1024, kHdr = kPar + 256;  // 1544
-constexpr int kRing = 20 * 1024;
-constexpr int kTickets = 8;
-constexpr int kCW = 4;
-constexpr int kThreads = (kCW + 1) * 32;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -61,17 +55,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// try_wait with a suspend-time hint: the thread sleeps until the phase
-// completes (or the hint expires) instead of spinning on the issue port.
+// Wait for an mbarrier phase (the block normally is already there).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -83,9 +76,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32) : "memory");
 }
 // A fragment of m16n8k32 (rows = bytes of 16-byte smem rows, k = smem rows),
 // i.e. a byte transpose of 32 smem rows; lane L gives the address of row L.
@@ -267,102 +257,146 @@ __device__ __forceinline__ void build_desc(const Chunk& ch, int lane, uint32_t* 
 
 // ---------------------------------------------------------------- work split
 // The layer's blocks are numbered gb = u * NB + j (unit u = b * H + h, block j,
-// NB = blocks per sequence; sequences advance in lockstep).  CTA c of a grid of
-// N owns the contiguous range [T*c/N, T*(c+1)/N) of the T = U*NB blocks, so
-// every CTA gets the same work to within one block (no tail of idle SMs), and
-// a range spans only a few units.  Ticket t of a CTA is block b0 + t; consumer
-// warp w takes tickets w, w + kCW, ...
+// NB = blocks per sequence; sequences advance in lockstep).  Warp W of the
+// N = grid * warps-per-CTA warps owns the contiguous range [T*W/N, T*(W+1)/N)
+// of the T = U*NB blocks: every warp gets the same work to within one block
+// (no tail of idle SMs) and a range spans only a few units.  Warps are
+// independent: each streams its own blocks into its own shared-memory ring.
 struct Range {
   int64_t b0, b1;
 };
-__device__ __forceinline__ Range cta_range(int64_t total) {
+__host__ __device__ __forceinline__ Range warp_range(int64_t total, int64_t wid, int64_t nwarps) {
   Range r;
-  r.b0 = total * blockIdx.x / gridDim.x;
-  r.b1 = total * (blockIdx.x + 1) / gridDim.x;
+  r.b0 = total * wid / nwarps;
+  r.b1 = total * (wid + 1) / nwarps;
   return r;
 }
-__host__ __device__ __forceinline__ int64_t cta_of(int64_t gb, int64_t total, int grid) {
-  return ((gb + 1) * grid - 1) / total;
+// the warp whose range contains block gb
+__host__ __device__ __forceinline__ int64_t warp_of(int64_t gb, int64_t total, int64_t nwarps) {
+  return ((gb + 1) * nwarps - 1) / total;
 }
 
-// ---------------------------------------------------------------- ring
-struct Ring {
-  uint8_t* data;
-  uint64_t* full;
-  uint64_t* empty;
-  uint32_t* start;  // [kTickets] ring offset of each ticket's block
-  uint32_t* abs;    // [kTickets] producer-private absolute start
-  int64_t* soff;    // [32] producer-private block offsets (staged table)
-  int* slen;        // [32] byte length, -1 = no block (past nblk)
-};
-constexpr size_t kRingBytes = kRing + kTickets * 16 + kTickets * 8 + 32 * 12;
-
-__device__ __forceinline__ uint8_t* setup_ring(uint8_t* smem, Ring& R) {
-  R.data = smem;
-  R.full = (uint64_t*)(smem + kRing);
-  R.empty = R.full + kTickets;
-  R.start = (uint32_t*)(R.empty + kTickets);
-  R.abs = R.start + kTickets;
-  R.soff = (int64_t*)(R.abs + kTickets);
-  R.slen = (int*)(R.soff + 32);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kTickets; ++s) {
-      mbar_init(&R.full[s], 1);
-      mbar_init(&R.empty[s], 1);
-    }
-    fence_barrier_init();
+// Position (unit u, block j) of a global block index, advanced without division.
+struct Cursor {
+  int u, j;
+  __device__ __forceinline__ void init(int64_t gb, int NB) {
+    u = int(gb / NB);
+    j = int(gb - int64_t(u) * NB);
   }
-  return smem + kRingBytes;
-}
+  __device__ __forceinline__ void step(int by, int NB) {
+    j += by;
+    while (j >= NB) {
+      j -= NB;
+      ++u;
+    }
+  }
+};
 
-// Producer warp: stages 32 directory entries at a time (lane-parallel), then
-// lane 0 issues one TMA bulk copy per block into the ring (tickets in block
-// order).  A block past its sequence's nblk gets a plain arrive (no copy).
-__device__ void produce(const Ring& R, const pkv_layer_t& L, int kind, int NB, Range rg, int lane) {
-  const int U = L.batch * L.heads;
-  uint32_t head = 0;
-  int oldest = 0, ticket = 0;
-  for (int64_t g0 = rg.b0; g0 < rg.b1; g0 += 32) {
-    const int n = int((rg.b1 - g0 < 32 ? rg.b1 - g0 : 32));
-    if (lane < n) {
-      const int64_t gb = g0 + lane;
-      const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
-      const int64_t tab = (int64_t(kind) * U + u) * L.max_blocks + j;
-      const bool ok = j < L.nblk[u / L.heads];
-      R.soff[lane] = ok ? L.blk_off[tab] : 0;
-      R.slen[lane] = ok ? L.blk_len[tab] : -1;
+// ---------------------------------------------------------------- per-warp feed
+// A warp streams its blocks with 1-D TMA bulk copies into a private byte ring
+// of RB bytes with NS mbarrier slots.  Bulk copies issued by one warp are
+// serviced one after another (~0.4 us each for 4 KB; tools/probe/
+// tma_feed_probe.cu), so every consumer warp is its own producer: a CTA-wide
+// producer warp caps the feed at ~1.4 TB/s per CTA.  Blocks are issued up to
+// NS - 1 ahead, as soon as the ring has room; a block's bytes stay valid until
+// the warp is done with it.
+template <int RB, int NS>
+struct Feed {
+  uint8_t* ring;
+  uint64_t* bar;     // [NS] full barriers (count 1 + tx bytes)
+  uint32_t* pos;     // [NS] ring offset of the block in the slot
+  uint32_t* abs;     // [NS] absolute start (for space accounting)
+  const uint8_t** gsrc;  // [NS] non-null: block larger than the ring, read in place from global memory
+  uint32_t head;     // absolute allocation point
+  int issued;        // blocks issued so far
+  // directory of the warp's blocks, lane-distributed: entry k0 + lane
+  int k0;
+  int64_t offl;
+  int lenl;          // -1: no block (past nblk)
+
+  __device__ __forceinline__ void init(uint8_t* smem, int lane) {
+    ring = smem;
+    bar = (uint64_t*)(smem + RB);
+    gsrc = (const uint8_t**)(bar + NS);
+    pos = (uint32_t*)(gsrc + NS);
+    abs = pos + NS;
+    head = 0;
+    issued = 0;
+    k0 = -32;
+    if (lane == 0) {
+      for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+      fence_barrier_init();
     }
     __syncwarp();
+  }
+  static constexpr size_t bytes() { return RB + NS * 24; }
+
+  // (re)load the directory entries of the warp's blocks kk .. kk+31
+  __device__ __forceinline__ void load_dir(const pkv_layer_t& L, int kind, int NB, const Range& rg, int kk, int lane) {
+    k0 = kk;
+    const int64_t gb = rg.b0 + kk + lane;
+    offl = 0;
+    lenl = -1;
+    if (gb < rg.b1) {
+      const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
+      if (j < L.nblk[u / L.heads]) {
+        const int64_t tab = (int64_t(kind) * L.batch * L.heads + u) * L.max_blocks + j;
+        offl = L.blk_off[tab];
+        lenl = L.blk_len[tab];
+      }
+    }
+  }
+  // issue the warp's next block if the ring has room; false when it has not
+  __device__ __forceinline__ bool try_issue(const pkv_layer_t& L, int kind, int NB, const Range& rg, int nk,
+                                            uint32_t tail, int lane) {
+    if (issued >= nk) return false;
+    if (issued >= k0 + 32) load_dir(L, kind, NB, rg, issued, lane);
+    const int len = __shfl_sync(PKV_FULL, lenl, issued - k0);
+    const int64_t off = __shfl_sync(PKV_FULL, offl, issued - k0);
+    const bool big = len + 16 + 16 > RB;              // cannot be staged: read in place
+    const uint32_t bytes = (len < 0 || big) ? 0u : uint32_t((len + 15) & ~15);
+    const uint32_t size = (len < 0 || big) ? 0u : bytes + 16;  // +16: slack for the decoders' word over-reads
+    uint32_t p = head % RB, skip = 0;
+    if (p + size > RB) {
+      skip = RB - p;
+      p = 0;
+    }
+    if (head + skip + size - tail > RB) return false;
+    const int s = issued % NS;
     if (lane == 0) {
-      for (int i = 0; i < n; ++i, ++ticket) {
-        const int tk = ticket % kTickets;
-        const int len = R.slen[i];
-        const uint32_t bytes = len < 0 ? 0u : uint32_t((len + 15) & ~15);
-        const uint32_t size = len < 0 ? 0u : bytes + 16;  // +16: slack for the decoders' word over-reads
-        uint32_t pos = head % kRing;
-        if (pos + size > kRing) {
-          head += kRing - pos;
-          pos = 0;
-        }
-        while (oldest < ticket &&
-               ((ticket - oldest) >= kTickets || head + size - R.abs[oldest % kTickets] > kRing)) {
-          mbar_wait(&R.empty[oldest % kTickets], uint32_t((oldest / kTickets) & 1));
-          ++oldest;
-        }
-        R.abs[tk] = head;
-        R.start[tk] = pos;
-        if (len < 0) {
-          mbar_arrive(&R.full[tk]);
-        } else {
-          mbar_expect_tx(&R.full[tk], bytes);
-          tma_load_1d(R.data + pos, L.arena + R.soff[i], bytes, &R.full[tk]);
-        }
-        head += size;
+      pos[s] = p;
+      abs[s] = head + skip;
+      gsrc[s] = big ? L.arena + off : nullptr;
+      if (len < 0 || big) {
+        mbar_arrive(&bar[s]);
+      } else {
+        // the ring bytes being overwritten were last read through the generic proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], bytes);
+        tma_load_1d(ring + p, L.arena + off, bytes, &bar[s]);
       }
     }
     __syncwarp();
+    head += skip + size;
+    ++issued;
+    return true;
   }
-}
+  // oldest ring byte still needed once block k is finished
+  __device__ __forceinline__ uint32_t tail_after(int k) const { return k + 1 < issued ? abs[(k + 1) % NS] : head; }
+  // top up: issue while there is room and a free slot (at most NS - 1 ahead of k)
+  __device__ __forceinline__ void refill(const pkv_layer_t& L, int kind, int NB, const Range& rg, int nk, int k,
+                                         uint32_t tail, int lane) {
+    while (issued < nk && issued < k + NS && try_issue(L, kind, NB, rg, nk, tail, lane)) {
+    }
+  }
+  // wait for block k; returns its bytes
+  __device__ __forceinline__ const uint8_t* wait(int k) {
+    const int s = k % NS;
+    mbar_wait(&bar[s], uint32_t((k / NS) & 1));
+    const uint8_t* g = gsrc[s];
+    return g ? g : ring + pos[s];
+  }
+};
 
 // ======================================================================= K
 // Per-warp tile: [row-group g][channel c][16 bytes], row R = 128g + c at byte
@@ -370,6 +404,10 @@ __device__ void produce(const Ring& R, const pkv_layer_t& L, int kind, int NB, R
 // 128-byte line: each quarter-warp of a decode step's STS.128 and each 8-row
 // phase of the ldmatrix hit 8 distinct chunks, i.e. no bank conflicts).
 constexpr int kTile = 4 * 128 * 16;  // 8 KB
+constexpr int kWK = 4;               // warps per CTA
+constexpr int kRBK = 10 * 1024, kNSK = 3;
+using FeedK = Feed<kRBK, kNSK>;
+constexpr size_t kWarpSmemK = (kTile + FeedK::bytes() + 127) / 128 * 128;
 
 __device__ __forceinline__ float sel8(const float (&v)[8], int i) {
   float r = v[0];
@@ -450,25 +488,21 @@ __device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G,
     }
 }
 
+
 template <int NU>  // unsigned query digit tiles: 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kThreads, 4) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
-                                                                    float* __restrict__ scores, int64_t sstride, int NB,
-                                                                    int64_t total) {
+__global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
+                                                                 float* __restrict__ scores, int64_t sstride, int NB,
+                                                                 int64_t total) {
   extern __shared__ __align__(128) uint8_t smem[];
-  Ring R;
-  uint8_t* rest = setup_ring(smem, R);
-  uint8_t* tiles = rest;                       // [kCW][kTile]
-  uint4* lut = (uint4*)(tiles + kCW * kTile);  // [16]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gi = lane >> 2, tq = lane & 3;
   const int U = L.batch * L.heads, Hq = L.heads * G;
-  const Range rg = cta_range(total);
+  uint4* lut = (uint4*)smem;  // [16]
   init_lut(lut, threadIdx.x);
+  uint8_t* wsm = smem + 256 + warp * kWarpSmemK;
+  uint8_t* tile = wsm;
+  FeedK F;
+  F.init(wsm + kTile, lane);
   __syncthreads();
-  if (warp == kCW) {  // producer; no CTA-wide barrier follows
-    produce(R, L, 0, NB, rg, lane);
-    return;
-  }
-  uint8_t* tile = tiles + warp * kTile;
   const uint32_t tile_s = smem_u32(tile);
   const uint8_t* lutb = (const uint8_t*)lut;
   // STS offsets: lane l's pack i (physical 16l + i) is row-group l >> 3,
@@ -477,130 +511,135 @@ __global__ void __launch_bounds__(kThreads, 4) fused_k_fast_kernel(pkv_layer_t L
   const uint32_t X = 4u * (lane & 1);
   const uint32_t st_even = 16u * ((R0 & ~7u) | ((R0 & 7u) ^ X));
   const uint32_t st_odd = 16u * ((R0 & ~7u) | (((R0 & 7u) | 4u) ^ X));
-  QFrag<NU> F;
-  int cur_u = -1;
-  const int n = int(rg.b1 - rg.b0);
+  const int64_t nwarps = int64_t(gridDim.x) * kWK, wid = int64_t(blockIdx.x) * kWK + warp;
+  const Range rg = warp_range(total, wid, nwarps);
+  const int nk = int(rg.b1 - rg.b0);
+  QFrag<NU> Q;
+  int cur_u = -1, nbk = 0;
+  float* sbase = scores;
+  Cursor cs;
+  cs.init(rg.b0, NB);
+  F.refill(L, 0, NB, rg, nk, -1, 0u, lane);
 
 #pragma unroll 1
-  for (int t = warp; t < n; t += kCW) {
-    const int64_t gb = rg.b0 + t;
-    const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
-    const int b = u / L.heads, h = u - b * L.heads;
+  for (int k = 0; k < nk; ++k, cs.step(1, NB)) {
+    const int u = cs.u, j = cs.j;
     if (u != cur_u) {
-      build_qfrag<NU>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, F);
       cur_u = u;
+      const int b = u / L.heads, h = u - b * L.heads;
+      nbk = L.nblk[b];
+      sbase = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride;
+      build_qfrag<NU>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, Q);
     }
-    float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride + int64_t(j) * kRows;
-    const int tk = t % kTickets;
-    mbar_wait(&R.full[tk], uint32_t((t / kTickets) & 1));
-    if (j >= L.nblk[b]) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&R.empty[tk]);
-      continue;
-    }
-    const uint8_t* blk = R.data + R.start[tk];
-    Chunk ch;
-    const bool fast = parse_chunk(blk, lane, ch);
-    if (fast) {
-      uint32_t bit = ch.bit;
-      uint32_t w16 = w16_of(ch.nb, 0);
-      PackLd cur = pack_load(blk, lutb, bit, w16);
+    const uint8_t* blk = F.wait(k);
+    if (j < nbk) {
+      Chunk ch;
+      const bool fast = parse_chunk(blk, lane, ch);
+      if (fast) {
+        uint32_t bit = ch.bit;
+        uint32_t w16 = w16_of(ch.nb, 0);
+        PackLd cur = pack_load(blk, lutb, bit, w16);
 #pragma unroll
-      for (int i2 = 0; i2 < 16; ++i2) {
-        const uint32_t nbit = bit + w16;
-        const uint32_t nw16 = i2 < 15 ? w16_of(ch.nb, i2 + 1) : 0u;
-        PackLd nxt;
-        if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
-        uint32_t r[4];
-        pack_decode(cur, bit, min_rep(ch.mn, i2), r);
-        *(uint4*)(tile + ((i2 & 1) ? st_odd : st_even) + 128u * (i2 >> 1)) = make_uint4(r[0], r[1], r[2], r[3]);
-        bit = nbit;
-        w16 = nw16;
-        if (i2 < 15) cur = nxt;
-      }
-      // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
-      uint32_t prm[4][2];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        prm[g][0] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi)));
-        prm[g][1] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi) + 8));
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&R.empty[tk]);  // ring slot no longer read
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        int accU[NU][4], accS[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          accS[e] = 0;
-#pragma unroll
-          for (int nu = 0; nu < NU; ++nu) accU[nu][e] = 0;
+        for (int i2 = 0; i2 < 16; ++i2) {
+          const uint32_t nbit = bit + w16;
+          const uint32_t nw16 = i2 < 15 ? w16_of(ch.nb, i2 + 1) : 0u;
+          PackLd nxt;
+          if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
+          uint32_t r[4];
+          pack_decode(cur, bit, min_rep(ch.mn, i2), r);
+          *(uint4*)(tile + ((i2 & 1) ? st_odd : st_even) + 128u * (i2 >> 1)) = make_uint4(r[0], r[1], r[2], r[3]);
+          bit = nbit;
+          w16 = nw16;
+          if (i2 < 15) cur = nxt;
         }
-        // lane L addresses row R = 128g + 32jj + L
-        const uint32_t a0 = tile_s + 16u * (128u * g + lane);              // jj = 0, 1 (+512 B)
-        const uint32_t a1 = tile_s + 16u * (128u * g + (lane ^ 4u) + 64u);  // jj = 2, 3
+        // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
+        uint32_t prm[4][2];
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          uint32_t a[4];
-          ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
+        for (int g = 0; g < 4; ++g) {
+          prm[g][0] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi)));
+          prm[g][1] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi) + 8));
+        }
+        __syncwarp();
+        float* p0 = sbase + int64_t(tq) * sstride + j * kRows + tok(gi);  // rows 16g + tok(gi) (+8) of head tq
+        float* p1 = p0 + 4 * sstride;                                     // head tq + 4
 #pragma unroll
-          for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, F.u[nu][jj][0], F.u[nu][jj][1]);
-          imma_us(accS, a, F.s[jj][0], F.s[jj][1]);
-        }
-        const int tA = 16 * g + tok(gi), tB = tA + 8;
-        const float sA = h2f(prm[g][0] & 0xffff), zA = h2f(prm[g][0] >> 16);
-        const float sB = h2f(prm[g][1] & 0xffff), zB = h2f(prm[g][1] >> 16);
-        if (tq < G) {
-          const float vA = float(accU[0][0]) + 256.f * float(accU[0][1]) + 65536.f * float(accS[0]);
-          const float vB = float(accU[0][2]) + 256.f * float(accU[0][3]) + 65536.f * float(accS[2]);
-          srow[int64_t(tq) * sstride + tA] = fmaf(sA, vA * F.inv[0], zA * F.qs[0]);
-          srow[int64_t(tq) * sstride + tB] = fmaf(sB, vB * F.inv[0], zB * F.qs[0]);
-        }
-        if (NU == 2 && tq + 4 < G) {
-          const float vA = float(accU[NU - 1][0]) + 256.f * float(accU[NU - 1][1]) + 65536.f * float(accS[1]);
-          const float vB = float(accU[NU - 1][2]) + 256.f * float(accU[NU - 1][3]) + 65536.f * float(accS[3]);
-          srow[int64_t(tq + 4) * sstride + tA] = fmaf(sA, vA * F.inv[1], zA * F.qs[1]);
-          srow[int64_t(tq + 4) * sstride + tB] = fmaf(sB, vB * F.inv[1], zB * F.qs[1]);
-        }
-      }
-      __syncwarp();  // tile reads done before the next block's stores
-    } else {
-      // scalar path (rare): lane computes rows lane and lane+32 for every head
-      const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
-      uint32_t* desc = (uint32_t*)tile;
-      build_desc(ch, lane, desc);
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        const int tt = lane + 32 * half, rgp = tt >> 4, t16 = tt & 15;
-        const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * tt);
-        const float s = h2f(pr & 0xffff), z = h2f(pr >> 16);
-#pragma unroll 1
-        for (int g = 0; g < G; ++g) {
-          float acc = 0.f, qsum = 0.f;
-#pragma unroll 1
-          for (int pos = 0; pos < 128; ++pos) {
-            const uint32_t d = desc[rgp * 128 + pos];
-            const uint32_t wd = d >> 18;
-            const float code = float(pack_min(blk, rgp * 128 + pos) + field_at(blk, (d & 0x3ffffu) + t16 * wd, wd));
-            const float qc = qu[g * kD + kpos_to_col(pos, kD)];
-            acc = fmaf(code, qc, acc);
-            qsum += qc;
+        for (int g = 0; g < 4; ++g) {
+          int accU[NU][4], accS[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            accS[e] = 0;
+#pragma unroll
+            for (int nu = 0; nu < NU; ++nu) accU[nu][e] = 0;
           }
-          srow[int64_t(g) * sstride + tt] = fmaf(s, acc, z * qsum);
+          // lane L addresses row R = 128g + 32jj + L
+          const uint32_t a0 = tile_s + 16u * (128u * g + lane);              // jj = 0, 1 (+512 B)
+          const uint32_t a1 = tile_s + 16u * (128u * g + (lane ^ 4u) + 64u);  // jj = 2, 3
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            uint32_t a[4];
+            ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
+#pragma unroll
+            for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, Q.u[nu][jj][0], Q.u[nu][jj][1]);
+            imma_us(accS, a, Q.s[jj][0], Q.s[jj][1]);
+          }
+          const float sA = h2f(prm[g][0] & 0xffff), zA = h2f(prm[g][0] >> 16);
+          const float sB = h2f(prm[g][1] & 0xffff), zB = h2f(prm[g][1] >> 16);
+          // digit sums: d0 + 256*d1 <= 128*255*65535 < 2^31 is exact in int32
+          if (tq < G) {
+            const float vA = fmaf(65536.f, float(accS[0]), float(accU[0][0] + 256 * accU[0][1]));
+            const float vB = fmaf(65536.f, float(accS[2]), float(accU[0][2] + 256 * accU[0][3]));
+            p0[16 * g] = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]);
+            p0[16 * g + 8] = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
+          }
+          if (NU == 2 && tq + 4 < G) {
+            const float vA = fmaf(65536.f, float(accS[1]), float(accU[NU - 1][0] + 256 * accU[NU - 1][1]));
+            const float vB = fmaf(65536.f, float(accS[3]), float(accU[NU - 1][2] + 256 * accU[NU - 1][3]));
+            p1[16 * g] = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]);
+            p1[16 * g + 8] = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
+          }
         }
+        __syncwarp();  // tile reads done before the next block's stores
+      } else {
+        // scalar path (rare): lane computes rows lane and lane+32 for every head
+        const int b = u / L.heads, h = u - b * L.heads;
+        const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
+        float* srow = sbase + j * kRows;
+        uint32_t* desc = (uint32_t*)tile;
+        build_desc(ch, lane, desc);
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          const int tt = lane + 32 * half, rgp = tt >> 4, t16 = tt & 15;
+          const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * tt);
+          const float s = h2f(pr & 0xffff), z = h2f(pr >> 16);
+#pragma unroll 1
+          for (int g = 0; g < G; ++g) {
+            float acc = 0.f, qsum = 0.f;
+#pragma unroll 1
+            for (int pos = 0; pos < 128; ++pos) {
+              const uint32_t d = desc[rgp * 128 + pos];
+              const uint32_t wd = d >> 18;
+              const float code = float(pack_min(blk, rgp * 128 + pos) + field_at(blk, (d & 0x3ffffu) + t16 * wd, wd));
+              const float qc = qu[g * kD + kpos_to_col(pos, kD)];
+              acc = fmaf(code, qc, acc);
+              qsum += qc;
+            }
+            srow[int64_t(g) * sstride + tt] = fmaf(s, acc, z * qsum);
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&R.empty[tk]);
     }
+    F.refill(L, 0, NB, rg, nk, k, F.tail_after(k), lane);
   }
-  // uncompressed residue rows of units u = blockIdx.x, blockIdx.x + grid, ...
-  for (int u = blockIdx.x; u < U; u += gridDim.x) {
+  // uncompressed residue rows of units u = wid, wid + nwarps, ...
+  for (int64_t uu = wid; uu < U; uu += nwarps) {
+    const int u = int(uu);
     const int b = u / L.heads, h = u - b * L.heads;
     const int nr = L.nres[b];
     const uint16_t* kr = L.stage + (int64_t(0) * U + u) * L.buffer * kD;
     const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
     float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride + int64_t(L.nblk[b]) * kRows;
-    for (int t = warp; t < nr; t += kCW) {
+    for (int t = 0; t < nr; ++t) {
       for (int g = 0; g < G; ++g) {
         float a = 0.f;
         for (int c = lane; c < kD; c += 32) a = fmaf(__half2float(__ushort_as_half(kr[t * kD + c])), qu[g * kD + c], a);
@@ -618,43 +657,45 @@ __global__ void __launch_bounds__(kThreads, 4) fused_k_fast_kernel(pkv_layer_t L
 // / 8..11 (k-step 1), chunk tq+4 <-> bytes 4..7 / 12..15.  The B operand
 // (rows x [head, digit]) comes from a per-warp [head][digit][64] byte array
 // in the same byte order.  D columns 2tq, 2tq+1 = head tq digits 0, 1, so lane
-// (gi, tq) owns out[head 4nt + tq][channels 16gi .. 16gi+15].  Per (CTA range
-// segment = unit, warp) partial sums go to scratch; the finalize kernel adds
+// (gi, tq) owns out[head 4nt + tq][channels 16gi .. 16gi+15].  Per (warp,
+// range segment = unit) partial sums go to scratch; the finalize kernel adds
 // them in a fixed order (deterministic) plus the residue.
 constexpr int kPart = kD + 4;  // 128 channels, the z term, padding (16-byte rows)
+constexpr int kWV = 4;
+constexpr int kRBV = 10 * 1024, kNSV = 3;
+using FeedV = Feed<kRBV, kNSV>;
+constexpr size_t kWarpSmemV = (2048 + FeedV::bytes() + 127) / 128 * 128;
 
 template <int NT>  // n-tiles: 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kThreads, 4) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
-                                                                    int64_t wstride, float* __restrict__ part, int NB,
-                                                                    int64_t total, int maxseg,
-                                                                    float* __restrict__ vscr) {
+__global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
+                                                                 int64_t wstride, float* __restrict__ part, int NB,
+                                                                 int64_t total, int maxseg,
+                                                                 float* __restrict__ vscr) {
   constexpr int GP = 4 * NT;    // padded heads
   constexpr int LPH = 32 / GP;  // writer lanes per head
   constexpr int TPL = 64 / LPH; // rows per writer lane (8 or 16)
   extern __shared__ __align__(128) uint8_t smem[];
-  Ring R;
-  uint8_t* rest = setup_ring(smem, R);
-  uint32_t* desc_all = (uint32_t*)rest;                  // [kCW][512] (slow path)
-  uint8_t* frag_all = (uint8_t*)(desc_all + kCW * 512);  // [kCW][GP][2][64]
-  uint4* lut = (uint4*)(frag_all + kCW * GP * 128);      // [16]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gi = lane >> 2, tq = lane & 3;
   const int Hq = L.heads * G;
-  const Range rg = cta_range(total);
+  uint4* lut = (uint4*)smem;  // [16]
   init_lut(lut, threadIdx.x);
+  uint8_t* wsm = smem + 256 + warp * kWarpSmemV;
+  // 2 KB: the B operand staging [GP][2][64] (<= 1 KB), reused as the slow
+  // path's descriptor table [512] after the B fragments are in registers
+  uint32_t* desc = (uint32_t*)wsm;
+  uint8_t* frag = wsm;
+  FeedV F;
+  F.init(wsm + 2048, lane);
   __syncthreads();
-  if (warp == kCW) {
-    produce(R, L, 1, NB, rg, lane);
-    return;
-  }
-  uint32_t* desc = desc_all + warp * 512;
-  uint8_t* frag = frag_all + warp * GP * 128;
   const uint8_t* lutb = (const uint8_t*)lut;
-  float* vsl = vscr + (int64_t(blockIdx.x) * kCW + warp) * (8 * kD);  // scalar-path partials [8][kD]
+  const int64_t nwarps = int64_t(gridDim.x) * kWV, wid = int64_t(blockIdx.x) * kWV + warp;
+  float* vsl = vscr + wid * (8 * kD);  // scalar-path partials [8][kD]
   // writer role for the B operand: head wh, rows wt0 .. wt0 + TPL - 1
   const int wh = lane / LPH, wt0 = (lane % LPH) * TPL;
-  const int n = int(rg.b1 - rg.b0);
+  const Range rg = warp_range(total, wid, nwarps);
+  const int nk = int(rg.b1 - rg.b0);
   const int u_first = int(rg.b0 / NB);
-  const int u_last = n > 0 ? int((rg.b1 - 1) / NB) : u_first - 1;
+  const int u_last = nk > 0 ? int((rg.b1 - 1) / NB) : u_first - 1;
 
   float acc[NT][16];
   float zacc = 0.f;
@@ -666,7 +707,10 @@ __global__ void __launch_bounds__(kThreads, 4) fused_v_fast_kernel(pkv_layer_t L
     for (int i = 0; i < 16; ++i) acc[nt][i] = 0.f;
   // write the accumulators of segment `seg` (then zero them)
   auto flush = [&]() {
-    float* pp = part + ((int64_t(blockIdx.x) * maxseg + seg) * kCW + warp) * G * kPart;
+    // partials of unit u go to slot (this warp - first warp covering u) of the unit
+    const int u = u_first + seg;
+    const int64_t slot = wid - warp_of(int64_t(u) * NB, total, nwarps);
+    float* pp = part + (int64_t(u) * maxseg + slot) * G * kPart;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int g = 4 * nt + tq;
@@ -695,14 +739,13 @@ __global__ void __launch_bounds__(kThreads, 4) fused_v_fast_kernel(pkv_layer_t L
     }
     ++seg;
   };
-  // weights of this warp's first block (prefetched one block ahead)
+
+  // weights of the next block (prefetched one block ahead)
   float wn[TPL];
-  auto load_w = [&](int t) {
-    const int64_t gb = rg.b0 + t;
-    const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
-    const int b = u / L.heads, h = u - b * L.heads;
-    const float* wrow = w + (int64_t(b) * Hq + int64_t(h) * G + wh) * wstride + int64_t(j) * kRows + wt0;
-    const bool ok = t < n && wh < G;
+  auto load_w = [&](int k, const Cursor& c) {
+    const int b = c.u / L.heads, h = c.u - b * L.heads;
+    const float* wrow = w + (int64_t(b) * Hq + int64_t(h) * G + wh) * wstride + int64_t(c.j) * kRows + wt0;
+    const bool ok = k < nk && wh < G;
 #pragma unroll
     for (int q4 = 0; q4 < TPL / 4; ++q4) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -710,179 +753,203 @@ __global__ void __launch_bounds__(kThreads, 4) fused_v_fast_kernel(pkv_layer_t L
       wn[4 * q4] = v.x; wn[4 * q4 + 1] = v.y; wn[4 * q4 + 2] = v.z; wn[4 * q4 + 3] = v.w;
     }
   };
-  load_w(warp);
+  Cursor cs, cn;
+  cs.init(rg.b0, NB);
+  cn = cs;
+  load_w(0, cn);
+  int cur_u = -1, b = 0, h = 0, nbk = 0;
+  F.refill(L, 1, NB, rg, nk, -1, 0u, lane);
 
 #pragma unroll 1
-  for (int t = warp; t < n; t += kCW) {
-    const int64_t gb = rg.b0 + t;
-    const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
-    const int b = u / L.heads, h = u - b * L.heads;
+  for (int k = 0; k < nk; ++k) {
+    const int u = cs.u, j = cs.j;
+    if (u != cur_u) {
+      cur_u = u;
+      b = u / L.heads;
+      h = u - b * L.heads;
+      nbk = L.nblk[b];
+    }
     while (seg < u - u_first) flush();
     float wc[TPL];
 #pragma unroll
     for (int e = 0; e < TPL; ++e) wc[e] = wn[e];
-    load_w(t + kCW);
-    const int tk = t % kTickets;
-    mbar_wait(&R.full[tk], uint32_t((t / kTickets) & 1));
-    if (j >= L.nblk[b]) {
+    cn.step(1, NB);
+    load_w(k + 1, cn);
+    cs = cn;
+    const uint8_t* blk = F.wait(k);
+    if (j < nbk) {
+      Chunk ch;
+      const bool fast = parse_chunk(blk, lane, ch);
+      // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits, f a power of two
+      // per (block, head) with max x * f < 2^16; z term sum_t w_t z_t in f32
+      float xs[TPL];
+      float mx = 0.f;
+#pragma unroll
+      for (int e2 = 0; e2 < TPL / 2; ++e2) {
+        const uint2 pr = *(const uint2*)(blk + kPar + 4 * (wt0 + 2 * e2));
+        const float s0 = h2f(pr.x & 0xffff), s1 = h2f(pr.y & 0xffff);
+        zacc = fmaf(wc[2 * e2], h2f(pr.x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr.y >> 16), zacc));
+        xs[2 * e2] = wc[2 * e2] * s0;
+        xs[2 * e2 + 1] = wc[2 * e2 + 1] * s1;
+        mx = fmaxf(mx, fmaxf(xs[2 * e2], xs[2 * e2 + 1]));
+      }
+#pragma unroll
+      for (int o = 1; o < LPH; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(PKV_FULL, mx, o));
+      // f = 2^(15 - e) for mx in [2^e, 2^(e+1)): mx * f < 2^16
+      const int eb = (__float_as_int(mx) >> 23) & 0xff;
+      const int fb = min(269 - eb, 254);
+      const float f = __int_as_float(fb << 23);
+      const float invf = __int_as_float((254 - fb) << 23);
+#pragma unroll
+      for (int e8 = 0; e8 < TPL / 8; ++e8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(__fmaf_rz(xs[8 * e8 + e], f, 8388608.f));
+        // byte position p holds row tok(p): (0,1,4,5) then (2,3,6,7)
+        const uint32_t t01 = __byte_perm(v[0], v[1], 0x5140), t45 = __byte_perm(v[4], v[5], 0x5140);
+        const uint32_t t23 = __byte_perm(v[2], v[3], 0x5140), t67 = __byte_perm(v[6], v[7], 0x5140);
+        const uint32_t lo0 = __byte_perm(t01, t45, 0x5410), hi0 = __byte_perm(t01, t45, 0x7632);
+        const uint32_t lo1 = __byte_perm(t23, t67, 0x5410), hi1 = __byte_perm(t23, t67, 0x7632);
+        *(uint2*)(frag + (wh * 2 + 0) * 64 + wt0 + 8 * e8) = make_uint2(lo0, lo1);
+        *(uint2*)(frag + (wh * 2 + 1) * 64 + wt0 + 8 * e8) = make_uint2(hi0, hi1);
+      }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&R.empty[tk]);
-      continue;
-    }
-    const uint8_t* blk = R.data + R.start[tk];
-    Chunk ch;
-    const bool fast = parse_chunk(blk, lane, ch);
-    // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits, f a power of two
-    // per (block, head) with max x * f < 2^16; z term sum_t w_t z_t in f32
-    float xs[TPL];
-    float mx = 0.f;
+      uint32_t bf[NT][4];
+      float inv[NT];
 #pragma unroll
-    for (int e2 = 0; e2 < TPL / 2; ++e2) {
-      const uint2 pr = *(const uint2*)(blk + kPar + 4 * (wt0 + 2 * e2));
-      const float s0 = h2f(pr.x & 0xffff), s1 = h2f(pr.y & 0xffff);
-      zacc = fmaf(wc[2 * e2], h2f(pr.x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr.y >> 16), zacc));
-      xs[2 * e2] = wc[2 * e2] * s0;
-      xs[2 * e2 + 1] = wc[2 * e2 + 1] * s1;
-      mx = fmaxf(mx, fmaxf(xs[2 * e2], xs[2 * e2 + 1]));
-    }
-#pragma unroll
-    for (int o = 1; o < LPH; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(PKV_FULL, mx, o));
-    // f = 2^(15 - e) for mx in [2^e, 2^(e+1)): mx * f < 2^16
-    const int eb = (__float_as_int(mx) >> 23) & 0xff;
-    const int fb = min(269 - eb, 254);
-    const float f = __int_as_float(fb << 23);
-    const float invf = __int_as_float((254 - fb) << 23);
-#pragma unroll
-    for (int e8 = 0; e8 < TPL / 8; ++e8) {
-      uint32_t v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(__fmaf_rz(xs[8 * e8 + e], f, 8388608.f));
-      // byte position p holds row tok(p): (0,1,4,5) then (2,3,6,7)
-      const uint32_t t01 = __byte_perm(v[0], v[1], 0x5140), t45 = __byte_perm(v[4], v[5], 0x5140);
-      const uint32_t t23 = __byte_perm(v[2], v[3], 0x5140), t67 = __byte_perm(v[6], v[7], 0x5140);
-      const uint32_t lo0 = __byte_perm(t01, t45, 0x5410), hi0 = __byte_perm(t01, t45, 0x7632);
-      const uint32_t lo1 = __byte_perm(t23, t67, 0x5410), hi1 = __byte_perm(t23, t67, 0x7632);
-      *(uint2*)(frag + (wh * 2 + 0) * 64 + wt0 + 8 * e8) = make_uint2(lo0, lo1);
-      *(uint2*)(frag + (wh * 2 + 1) * 64 + wt0 + 8 * e8) = make_uint2(hi0, hi1);
-    }
-    __syncwarp();
-    uint32_t bf[NT][4];
-    float inv[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const uint4 v = *(const uint4*)(frag + ((4 * nt + (gi >> 1)) * 2 + (gi & 1)) * 64 + 16 * tq);
-      bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
-      inv[nt] = __shfl_sync(PKV_FULL, invf, (4 * nt + tq) * LPH);
-    }
-    if (fast) {
-      // lane (gi, tq) = chunk 8tq + gi of the scan
-      const int src = 8 * tq + gi;
-      uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src);
-      const uint2 nb = *(const uint2*)(blk + kNib + 8 * src);
-      uint32_t mn[8];
-      {
-        const uint2* mp = (const uint2*)(blk + kMin + 32 * src);
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const uint2 v = mp[q4];
-          mn[2 * q4] = v.x;
-          mn[2 * q4 + 1] = v.y;
-        }
+      for (int nt = 0; nt < NT; ++nt) {
+        const uint4 v = *(const uint4*)(frag + ((4 * nt + (gi >> 1)) * 2 + (gi & 1)) * 64 + 16 * tq);
+        bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
+        inv[nt] = __shfl_sync(PKV_FULL, invf, (4 * nt + tq) * LPH);
       }
-      uint32_t w16 = w16_of(nb, 0);
-      PackLd cur = pack_load(blk, lutb, bit, w16);
+      __syncwarp();  // frag reads done (the slow path reuses the area)
+      if (fast) {
+        // lane (gi, tq) = chunk 8tq + gi of the scan
+        const int src = 8 * tq + gi;
+        uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src);
+        const uint2 nb = *(const uint2*)(blk + kNib + 8 * src);
+        uint32_t mn[8];
+        {
+          const uint2* mp = (const uint2*)(blk + kMin + 32 * src);
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        uint32_t P[2][4];
-#pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          const int i2 = 2 * mt + pp;
-          const uint32_t nbit = bit + w16;
-          const uint32_t nw16 = i2 < 15 ? w16_of(nb, i2 + 1) : 0u;
-          PackLd nxt;
-          if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
-          pack_decode(cur, bit, min_rep(mn, i2), P[pp]);
-          bit = nbit;
-          w16 = nw16;
-          if (i2 < 15) cur = nxt;
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint2 v = mp[q4];
+            mn[2 * q4] = v.x;
+            mn[2 * q4 + 1] = v.y;
+          }
         }
+        uint32_t w16 = w16_of(nb, 0);
+        PackLd cur = pack_load(blk, lutb, bit, w16);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          int d[4] = {0, 0, 0, 0};
-          const uint32_t a0[4] = {P[0][0], P[1][0], P[0][1], P[1][1]};
-          imma_uu(d, a0, bf[nt][0], bf[nt][1]);
-          const uint32_t a1[4] = {P[0][2], P[1][2], P[0][3], P[1][3]};
-          imma_uu(d, a1, bf[nt][2], bf[nt][3]);
-          acc[nt][2 * mt] = fmaf(float(d[0] + 256 * d[1]), inv[nt], acc[nt][2 * mt]);
-          acc[nt][2 * mt + 1] = fmaf(float(d[2] + 256 * d[3]), inv[nt], acc[nt][2 * mt + 1]);
+        for (int mt = 0; mt < 8; ++mt) {
+          uint32_t P[2][4];
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            const int i2 = 2 * mt + pp;
+            const uint32_t nbit = bit + w16;
+            const uint32_t nw16 = i2 < 15 ? w16_of(nb, i2 + 1) : 0u;
+            PackLd nxt;
+            if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
+            pack_decode(cur, bit, min_rep(mn, i2), P[pp]);
+            bit = nbit;
+            w16 = nw16;
+            if (i2 < 15) cur = nxt;
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            int d[4] = {0, 0, 0, 0};
+            const uint32_t a0[4] = {P[0][0], P[1][0], P[0][1], P[1][1]};
+            imma_uu(d, a0, bf[nt][0], bf[nt][1]);
+            const uint32_t a1[4] = {P[0][2], P[1][2], P[0][3], P[1][3]};
+            imma_uu(d, a1, bf[nt][2], bf[nt][3]);
+            acc[nt][2 * mt] = fmaf(float(d[0] + 256 * d[1]), inv[nt], acc[nt][2 * mt]);
+            acc[nt][2 * mt + 1] = fmaf(float(d[2] + 256 * d[3]), inv[nt], acc[nt][2 * mt + 1]);
+          }
         }
-      }
-    } else {
-      // scalar path (rare): lane owns channels lane + 32q, all 64 rows, all heads;
-      // partials accumulate in this warp's global scratch (fixed order, deterministic)
-      build_desc(ch, lane, desc);
-      if (!slow_used) {
-        for (int e = lane; e < 8 * kD; e += 32) vsl[e] = 0.f;
-        __syncwarp();
-        slow_used = true;
-      }
-      const float* wu = w + (int64_t(b) * Hq + int64_t(h) * G) * wstride + int64_t(j) * kRows;
-      float sacc[8][4];
+      } else {
+        // scalar path (rare): lane owns channels lane + 32q, all 64 rows, all heads;
+        // partials accumulate in this warp's global scratch (fixed order, deterministic)
+        build_desc(ch, lane, desc);
+        if (!slow_used) {
+          for (int e = lane; e < 8 * kD; e += 32) vsl[e] = 0.f;
+          __syncwarp();
+          slow_used = true;
+        }
+        const float* wu = w + (int64_t(b) * Hq + int64_t(h) * G) * wstride + int64_t(j) * kRows;
+        float sacc[8][4];
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
+        for (int g = 0; g < 8; ++g)
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) sacc[g][q4] = vsl[g * kD + lane + 32 * q4];
+          for (int q4 = 0; q4 < 4; ++q4) sacc[g][q4] = vsl[g * kD + lane + 32 * q4];
 #pragma unroll 1
-      for (int r = 0; r < kRows; ++r) {
-        const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * r);
-        const float s = h2f(pr & 0xffff);
-        float ws[8];
+        for (int r = 0; r < kRows; ++r) {
+          const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * r);
+          const float s = h2f(pr & 0xffff);
+          float ws[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) ws[g] = g < G ? wu[int64_t(g) * wstride + r] * s : 0.f;
-        const int rgp = r >> 4, tt = r & 15;
+          for (int g = 0; g < 8; ++g) ws[g] = g < G ? wu[int64_t(g) * wstride + r] * s : 0.f;
+          const int rgp = r >> 4, tt = r & 15;
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int c = lane + 32 * q4;
-          const uint32_t dd = desc[rgp * 128 + c];
-          const uint32_t wd = dd >> 18;
-          const float code = float(pack_min(blk, rgp * 128 + c) + field_at(blk, (dd & 0x3ffffu) + tt * wd, wd));
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int c = lane + 32 * q4;
+            const uint32_t dd = desc[rgp * 128 + c];
+            const uint32_t wd = dd >> 18;
+            const float code = float(pack_min(blk, rgp * 128 + c) + field_at(blk, (dd & 0x3ffffu) + tt * wd, wd));
 #pragma unroll
-          for (int g = 0; g < 8; ++g) sacc[g][q4] = fmaf(ws[g], code, sacc[g][q4]);
+            for (int g = 0; g < 8; ++g) sacc[g][q4] = fmaf(ws[g], code, sacc[g][q4]);
+          }
         }
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) vsl[g * kD + lane + 32 * q4] = sacc[g][q4];
       }
-#pragma unroll
-      for (int g = 0; g < 8; ++g)
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) vsl[g * kD + lane + 32 * q4] = sacc[g][q4];
+      __syncwarp();
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&R.empty[tk]);
+    F.refill(L, 1, NB, rg, nk, k, F.tail_after(k), lane);
   }
   while (seg <= u_last - u_first) flush();
 }
 
-// out[b][h*G+g][c] = sum over the CTAs whose range meets unit u (ascending),
-// their warps (ascending) of part, plus the z terms, plus the residue rows.
-__global__ void fused_v_fast_finalize(pkv_layer_t L, const float* __restrict__ part, const float* __restrict__ w,
-                                      int G, int64_t wstride, int NB, int64_t total, int grid, int maxseg,
-                                      float* __restrict__ out) {
+// out[b][h*G+g][c] = sum over the warps whose range meets unit u (ascending) of
+// their partials (channels and z term), plus the residue rows.  One CTA per
+// (unit, head): thread c < 128 owns channel c.
+__global__ void __launch_bounds__(128) fused_v_fast_finalize(pkv_layer_t L, const float* __restrict__ part,
+                                                              const float* __restrict__ w, int G, int64_t wstride,
+                                                              int NB, int64_t total, int64_t nwarps, int maxseg,
+                                                              float* __restrict__ out) {
   const int U = L.batch * L.heads;
-  const int64_t n = int64_t(U) * G * kD;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
-    const int c = int(e % kD);
-    const int64_t ug = e / kD;
-    const int g = int(ug % G);
-    const int u = int(ug / G);
+  const int c = threadIdx.x;
+  for (int ug = blockIdx.x; ug < U * G; ug += gridDim.x) {
+    const int u = ug / G, g = ug - u * G;
     float s = 0.f, z = 0.f;
     if (total > 0 && NB > 0) {
-      const int64_t c0 = cta_of(int64_t(u) * NB, total, grid), c1 = cta_of(int64_t(u + 1) * NB - 1, total, grid);
-      for (int64_t cc = c0; cc <= c1; ++cc) {
-        const int seg = u - int((total * cc / grid) / NB);
-        for (int wv = 0; wv < kCW; ++wv) {
-          const float* pp = part + ((cc * maxseg + seg) * kCW + wv) * G * kPart + g * kPart;
-          s += pp[c];
-          z += pp[kD];
+      const int64_t w0 = warp_of(int64_t(u) * NB, total, nwarps), w1 = warp_of(int64_t(u + 1) * NB - 1, total, nwarps);
+      const int ns = int(w1 - w0 + 1);
+      const float* pp = part + (int64_t(u) * maxseg * G + g) * kPart;
+      const int64_t st = int64_t(G) * kPart;
+      // 8 independent partial sums (loads in flight), combined in a fixed order
+      float a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = b[i] = 0.f;
+      int sl = 0;
+      for (; sl + 8 <= ns; sl += 8) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          a[i] += pp[(sl + i) * st + c];
+          b[i] += pp[(sl + i) * st + kD];
         }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (sl + i < ns) {
+          a[i] += pp[(sl + i) * st + c];
+          b[i] += pp[(sl + i) * st + kD];
+        }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s += a[i];
+        z += b[i];
       }
     }
     const int b = u / L.heads;
@@ -890,38 +957,51 @@ __global__ void fused_v_fast_finalize(pkv_layer_t L, const float* __restrict__ p
     const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
     const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
     for (int t = 0; t < nr; ++t) s = fmaf(wr[t], __half2float(__ushort_as_half(vr[t * kD + c])), s);
-    out[e] = s + z;
+    out[int64_t(ug) * kD + c] = s + z;
   }
 }
 
-constexpr size_t k_smem_bytes() { return kRingBytes + kCW * kTile + 16 * 16; }
-constexpr size_t v_smem_bytes() { return kRingBytes + kCW * 512 * 4 + kCW * 8 * 128 + 16 * 16; }
+constexpr size_t k_smem_bytes() { return 256 + kWK * kWarpSmemK; }
+constexpr size_t v_smem_bytes() { return 256 + kWV * kWarpSmemV; }
 
+// CTAs that fit on the device at once (queried once per kernel; the grid is
+// never larger, so every warp's range is resident for the whole launch)
 template <class K>
-int fast_grid(K kernel, size_t smem, int64_t total) {
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
+int fast_grid(K kernel, int threads, size_t smem, int64_t work_warps, int wpc) {
+  struct Cap {
+    const void* k;
+    int cap;
+  };
+  static Cap caps[8];
+  static int ncaps = 0;
+  int cap = 0;
+  for (int i = 0; i < ncaps; ++i)
+    if (caps[i].k == (const void*)kernel) cap = caps[i].cap;
+  if (!cap) {
+    int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+    cap = max(1, per) * nsm;
+    if (ncaps < 8) caps[ncaps++] = {(const void*)kernel, cap};
   }
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, smem);
-  const int64_t cap = int64_t(max(1, per)) * nsm;
-  return int(total < 1 ? 1 : (total < cap ? total : cap));
+  const int64_t want = (work_warps + wpc - 1) / wpc;
+  return int(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
 int v_grid(const pkv_layer_t* L, int nblocks, int G) {
   const int64_t total = int64_t(L->batch) * L->heads * nblocks;
-  return G <= 4 ? fast_grid(fused_v_fast_kernel<1>, v_smem_bytes(), total)
-                : fast_grid(fused_v_fast_kernel<2>, v_smem_bytes(), total);
+  return G <= 4 ? fast_grid(fused_v_fast_kernel<1>, kWV * 32, v_smem_bytes(), total, kWV)
+                : fast_grid(fused_v_fast_kernel<2>, kWV * 32, v_smem_bytes(), total, kWV);
 }
-int v_maxseg(const pkv_layer_t* L, int nblocks, int grid) {
+// slots per unit: the most warps whose ranges can meet one unit
+int v_maxseg(const pkv_layer_t* L, int nblocks, int64_t nwarps) {
   const int64_t total = int64_t(L->batch) * L->heads * nblocks;
   if (nblocks <= 0 || total <= 0) return 1;
-  const int64_t len = (total + grid - 1) / grid;
-  return int((len + nblocks - 1) / nblocks + 1);
+  const int64_t len_min = total / nwarps;  // every range has len_min or len_min + 1 blocks
+  if (len_min == 0) return int(nblocks < nwarps ? nblocks : nwarps) + 1;
+  return int((nblocks + len_min - 1) / len_min + 1);
 }
 
 }  // namespace
@@ -936,38 +1016,40 @@ int pkv_fast_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, f
   const int64_t total = int64_t(L->batch) * L->heads * nblocks;
   const int U = L->batch * L->heads;
   const int NB = max(1, nblocks);
+  const int64_t ww = total > U ? total : U;  // at least one warp per unit for the residue
   if (G <= 4) {
-    const int grid = fast_grid(fused_k_fast_kernel<1>, smem, total > U ? total : U);
-    fused_k_fast_kernel<1><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, NB, total);
+    const int grid = fast_grid(fused_k_fast_kernel<1>, kWK * 32, smem, ww, kWK);
+    fused_k_fast_kernel<1><<<grid, kWK * 32, smem, s>>>(*L, q, G, scores, sstride, NB, total);
   } else {
-    const int grid = fast_grid(fused_k_fast_kernel<2>, smem, total > U ? total : U);
-    fused_k_fast_kernel<2><<<grid, kThreads, smem, s>>>(*L, q, G, scores, sstride, NB, total);
+    const int grid = fast_grid(fused_k_fast_kernel<2>, kWK * 32, smem, ww, kWK);
+    fused_k_fast_kernel<2><<<grid, kWK * 32, smem, s>>>(*L, q, G, scores, sstride, NB, total);
   }
   return pkv_cuda_status(cudaGetLastError(), "pkv_fused_k_scores(fast)");
 }
 
 int64_t pkv_fast_v_scratch(const pkv_layer_t* L, int nblocks, int G) {
-  const int grid = v_grid(L, nblocks, G);
-  const int maxseg = v_maxseg(L, nblocks, grid);
-  return (int64_t(grid) * maxseg * kCW * G * kPart + int64_t(grid) * kCW * 8 * kD) * 4;
+  const int64_t nwarps = int64_t(v_grid(L, nblocks, G)) * kWV;
+  const int maxseg = v_maxseg(L, nblocks, nwarps);
+  return (int64_t(L->batch) * L->heads * maxseg * G * kPart + nwarps * 8 * kD) * 4;
 }
 
 int pkv_fast_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
                      float* part, cudaStream_t s) {
   const int64_t total = int64_t(L->batch) * L->heads * nblocks;
   const int grid = v_grid(L, nblocks, G);
-  const int maxseg = v_maxseg(L, nblocks, grid);
+  const int64_t nwarps = int64_t(grid) * kWV;
+  const int maxseg = v_maxseg(L, nblocks, nwarps);
   const int NB = max(1, nblocks);
-  float* vscr = part + int64_t(grid) * maxseg * kCW * G * kPart;
+  float* vscr = part + int64_t(L->batch) * L->heads * maxseg * G * kPart;
   const size_t smem = v_smem_bytes();
   if (total > 0) {
     if (G <= 4)
-      fused_v_fast_kernel<1><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
+      fused_v_fast_kernel<1><<<grid, kWV * 32, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
     else
-      fused_v_fast_kernel<2><<<grid, kThreads, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
+      fused_v_fast_kernel<2><<<grid, kWV * 32, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
   }
-  const int64_t n = int64_t(L->batch) * L->heads * G * kD;
-  const int fgrid = int((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
-  fused_v_fast_finalize<<<fgrid, 256, 0, s>>>(*L, part, w, G, wstride, NB, total, grid, maxseg, out);
+  const int ug = L->batch * L->heads * G;
+  fused_v_fast_finalize<<<ug < 148 * 16 ? ug : 148 * 16, 128, 0, s>>>(*L, part, w, G, wstride, NB, total, nwarps, maxseg,
+                                                                        out);
   return pkv_cuda_status(cudaGetLastError(), "pkv_fused_v_output(fast)");
 }
