@@ -361,7 +361,10 @@ struct Feed {
       skip = RB - p;
       p = 0;
     }
-    if (head + skip + size - tail > RB) return false;
+    // the skipped tail bytes are never live: with nothing in flight the block
+    // can always start at offset 0
+    const uint32_t live = tail == head ? head + skip : tail;
+    if (head + skip + size - live > RB) return false;
     const int s = issued % NS;
     if (lane == 0) {
       pos[s] = p;
@@ -389,12 +392,14 @@ struct Feed {
     while (issued < nk && issued < k + NS && try_issue(L, kind, NB, rg, nk, tail, lane)) {
     }
   }
-  // wait for block k; returns its bytes
-  __device__ __forceinline__ const uint8_t* wait(int k) {
+  // wait for block k; returns its bytes in the ring, or sets *g to the block
+  // in global memory when it was too large to stage (then the ring pointer is
+  // meaningless)
+  __device__ __forceinline__ const uint8_t* wait(int k, const uint8_t** g) {
     const int s = k % NS;
     mbar_wait(&bar[s], uint32_t((k / NS) & 1));
-    const uint8_t* g = gsrc[s];
-    return g ? g : ring + pos[s];
+    *g = gsrc[s];
+    return ring + pos[s];
   }
 };
 
@@ -405,7 +410,10 @@ struct Feed {
 // phase of the ldmatrix hit 8 distinct chunks, i.e. no bank conflicts).
 constexpr int kTile = 4 * 128 * 16;  // 8 KB
 constexpr int kWK = 4;               // warps per CTA
-constexpr int kRBK = 10 * 1024, kNSK = 3;
+#ifndef PKV_RBK
+#define PKV_RBK 10
+#endif
+constexpr int kRBK = PKV_RBK * 1024, kNSK = 3;
 using FeedK = Feed<kRBK, kNSK>;
 constexpr size_t kWarpSmemK = (kTile + FeedK::bytes() + 127) / 128 * 128;
 
@@ -531,26 +539,40 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
       sbase = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride;
       build_qfrag<NU>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, Q);
     }
-    const uint8_t* blk = F.wait(k);
+    const uint8_t* gblk;
+    const uint8_t* blk = F.wait(k, &gblk);
     if (j < nbk) {
       Chunk ch;
-      const bool fast = parse_chunk(blk, lane, ch);
+      const bool fast = gblk == nullptr && parse_chunk(blk, lane, ch);
       if (fast) {
+        // packs in pairs (two independent decode chains), loads one pair ahead
         uint32_t bit = ch.bit;
-        uint32_t w16 = w16_of(ch.nb, 0);
-        PackLd cur = pack_load(blk, lutb, bit, w16);
+        uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
+        PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
 #pragma unroll
-        for (int i2 = 0; i2 < 16; ++i2) {
-          const uint32_t nbit = bit + w16;
-          const uint32_t nw16 = i2 < 15 ? w16_of(ch.nb, i2 + 1) : 0u;
-          PackLd nxt;
-          if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
-          uint32_t r[4];
-          pack_decode(cur, bit, min_rep(ch.mn, i2), r);
-          *(uint4*)(tile + ((i2 & 1) ? st_odd : st_even) + 128u * (i2 >> 1)) = make_uint4(r[0], r[1], r[2], r[3]);
+        for (int i2 = 0; i2 < 16; i2 += 2) {
+          const uint32_t bitA = bit, bitB = bit + wa;
+          const uint32_t nbit = bitB + wb;
+          uint32_t nwa = 0, nwb = 0;
+          PackLd nA, nB;
+          if (i2 < 14) {
+            nwa = w16_of(ch.nb, i2 + 2);
+            nwb = w16_of(ch.nb, i2 + 3);
+            nA = pack_load(blk, lutb, nbit, nwa);
+            nB = pack_load(blk, lutb, nbit + nwa, nwb);
+          }
+          uint32_t ra[4], rb[4];
+          pack_decode(A, bitA, min_rep(ch.mn, i2), ra);
+          pack_decode(B, bitB, min_rep(ch.mn, i2 + 1), rb);
+          *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+          *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
           bit = nbit;
-          w16 = nw16;
-          if (i2 < 15) cur = nxt;
+          wa = nwa;
+          wb = nwb;
+          if (i2 < 14) {
+            A = nA;
+            B = nB;
+          }
         }
         // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
         uint32_t prm[4][2];
@@ -605,6 +627,10 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
         const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
         float* srow = sbase + j * kRows;
         uint32_t* desc = (uint32_t*)tile;
+        if (gblk) {
+          blk = gblk;
+          parse_chunk(blk, lane, ch);
+        }
         build_desc(ch, lane, desc);
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
@@ -776,10 +802,14 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
     cn.step(1, NB);
     load_w(k + 1, cn);
     cs = cn;
-    const uint8_t* blk = F.wait(k);
-    if (j < nbk) {
+    const uint8_t* gblk;
+    const uint8_t* sblk = F.wait(k, &gblk);
+    // one block: B operand, then the IMMA fast path or the scalar path.  Called
+    // with the shared-memory copy (LDS), or for a block too large to stage with
+    // the global-memory block (generic loads, scalar path only).
+    auto process = [&](const uint8_t* blk, bool may_fast) {
       Chunk ch;
-      const bool fast = parse_chunk(blk, lane, ch);
+      const bool fast = parse_chunk(blk, lane, ch) && may_fast;
       // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits, f a power of two
       // per (block, head) with max x * f < 2^16; z term sum_t w_t z_t in f32
       float xs[TPL];
@@ -838,22 +868,33 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
             mn[2 * q4 + 1] = v.y;
           }
         }
-        uint32_t w16 = w16_of(nb, 0);
-        PackLd cur = pack_load(blk, lutb, bit, w16);
+        // the m-tile's two packs decoded together, the next pair's loads in flight
+        uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
+        PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
           uint32_t P[2][4];
-#pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {
-            const int i2 = 2 * mt + pp;
-            const uint32_t nbit = bit + w16;
-            const uint32_t nw16 = i2 < 15 ? w16_of(nb, i2 + 1) : 0u;
-            PackLd nxt;
-            if (i2 < 15) nxt = pack_load(blk, lutb, nbit, nw16);
-            pack_decode(cur, bit, min_rep(mn, i2), P[pp]);
+          {
+            const int i2 = 2 * mt;
+            const uint32_t bitA = bit, bitB = bit + wa;
+            const uint32_t nbit = bitB + wb;
+            uint32_t nwa = 0, nwb = 0;
+            PackLd nA, nB;
+            if (i2 < 14) {
+              nwa = w16_of(nb, i2 + 2);
+              nwb = w16_of(nb, i2 + 3);
+              nA = pack_load(blk, lutb, nbit, nwa);
+              nB = pack_load(blk, lutb, nbit + nwa, nwb);
+            }
+            pack_decode(A, bitA, min_rep(mn, i2), P[0]);
+            pack_decode(B, bitB, min_rep(mn, i2 + 1), P[1]);
             bit = nbit;
-            w16 = nw16;
-            if (i2 < 15) cur = nxt;
+            wa = nwa;
+            wb = nwb;
+            if (i2 < 14) {
+              A = nA;
+              B = nB;
+            }
           }
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
@@ -905,6 +946,12 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
           for (int q4 = 0; q4 < 4; ++q4) vsl[g * kD + lane + 32 * q4] = sacc[g][q4];
       }
       __syncwarp();
+    };
+    if (j < nbk) {
+      if (gblk)
+        process(gblk, false);
+      else
+        process(sblk, true);
     }
     F.refill(L, 1, NB, rg, nk, k, F.tail_after(k), lane);
   }
