@@ -123,6 +123,31 @@ __device__ __forceinline__ uint32_t shf_r_clamp(uint32_t lo, uint32_t hi, uint32
   return d;
 }
 
+// Block reads.  Blocks staged in shared memory are addressed with 32-bit
+// shared-window addresses (LDS, no generic-address arithmetic); a block too
+// large to stage is read in place through a generic pointer.  The shared loads
+// are not volatile: their addresses derive from the slot offset read after the
+// slot's mbarrier wait, so they cannot be scheduled before it.
+__device__ __forceinline__ uint32_t ld32(const uint8_t* p) { return *(const uint32_t*)p; }
+__device__ __forceinline__ uint2 ld64(const uint8_t* p) { return *(const uint2*)p; }
+__device__ __forceinline__ uint32_t ld32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 ld64(uint32_t a) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 ld128(uint32_t a) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ const uint8_t* gptr(const uint8_t* p) { return p; }
+__device__ __forceinline__ const uint8_t* gptr(uint32_t a) { return (const uint8_t*)__cvta_shared_to_generic(a); }
+
 // ---------------------------------------------------------------- unpack
 // Per-width constants (w <= 4): MA = 2^(16-4w), MB = 2^(32-2w), MC = 2^(8-w),
 // byte mask (2^w - 1) * 0x01010101.  Entry w at lut + 16*w.
@@ -161,14 +186,14 @@ struct PackLd {
   uint32_t w0, w1, w2;
   uint4 c;
 };
-__device__ __forceinline__ PackLd pack_load(const uint8_t* __restrict__ blk, const uint8_t* __restrict__ lutb,
-                                            uint32_t bit, uint32_t w16) {
-  const uint32_t* p = (const uint32_t*)blk + (bit >> 5);
+template <class P>
+__device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ lut, uint32_t bit, uint32_t w16) {
+  const P p = blk + ((bit >> 5) << 2);
   PackLd r;
-  r.w0 = p[0];
-  r.w1 = p[1];
-  r.w2 = p[2];
-  r.c = *(const uint4*)(lutb + w16);
+  r.w0 = ld32(p);
+  r.w1 = ld32(p + 4);
+  r.w2 = ld32(p + 8);
+  r.c = *(const uint4*)(lut + w16);
   return r;
 }
 // r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
@@ -214,13 +239,13 @@ struct Chunk {
   uint32_t mn[8]; // 16 u16 minima
   uint32_t bit;   // payload bit offset of the chunk's first pack
 };
-__device__ __forceinline__ bool parse_chunk(const uint8_t* __restrict__ blk, int lane, Chunk& ch) {
-  ch.nb = *(const uint2*)(blk + kNib + 8 * lane);
-  const uint2* mp = (const uint2*)(blk + kMin + 32 * lane);
+template <class P>
+__device__ __forceinline__ bool parse_chunk(P blk, int lane, Chunk& ch) {
+  ch.nb = ld64(blk + kNib + 8 * lane);
   uint32_t mor = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint2 v = mp[q];
+    const uint2 v = ld64(blk + kMin + 32 * lane + 8 * q);
     ch.mn[2 * q] = v.x;
     ch.mn[2 * q + 1] = v.y;
     mor |= v.x | v.y;
@@ -395,11 +420,11 @@ struct Feed {
   // wait for block k; returns its bytes in the ring, or sets *g to the block
   // in global memory when it was too large to stage (then the ring pointer is
   // meaningless)
-  __device__ __forceinline__ const uint8_t* wait(int k, const uint8_t** g) {
+  __device__ __forceinline__ uint32_t wait(int k, const uint8_t** g) {
     const int s = k % NS;
     mbar_wait(&bar[s], uint32_t((k / NS) & 1));
     *g = gsrc[s];
-    return ring + pos[s];
+    return smem_u32(ring) + pos[s];
   }
 };
 
@@ -540,7 +565,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
       build_qfrag<NU>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, Q);
     }
     const uint8_t* gblk;
-    const uint8_t* blk = F.wait(k, &gblk);
+    const uint32_t blk = F.wait(k, &gblk);
     if (j < nbk) {
       Chunk ch;
       const bool fast = gblk == nullptr && parse_chunk(blk, lane, ch);
@@ -578,8 +603,8 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
         uint32_t prm[4][2];
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          prm[g][0] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi)));
-          prm[g][1] = *(const uint32_t*)(blk + kPar + 4 * (16 * g + tok(gi) + 8));
+          prm[g][0] = ld32(blk + kPar + 4 * (16 * g + tok(gi)));
+          prm[g][1] = ld32(blk + kPar + 4 * (16 * g + tok(gi) + 8));
         }
         __syncwarp();
         float* p0 = sbase + int64_t(tq) * sstride + j * kRows + tok(gi);  // rows 16g + tok(gi) (+8) of head tq
@@ -627,15 +652,13 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
         const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
         float* srow = sbase + j * kRows;
         uint32_t* desc = (uint32_t*)tile;
-        if (gblk) {
-          blk = gblk;
-          parse_chunk(blk, lane, ch);
-        }
+        const uint8_t* bg = gblk ? gblk : gptr(blk);
+        if (gblk) parse_chunk(bg, lane, ch);
         build_desc(ch, lane, desc);
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
           const int tt = lane + 32 * half, rgp = tt >> 4, t16 = tt & 15;
-          const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * tt);
+          const uint32_t pr = ld32(bg + kPar + 4 * tt);
           const float s = h2f(pr & 0xffff), z = h2f(pr >> 16);
 #pragma unroll 1
           for (int g = 0; g < G; ++g) {
@@ -644,7 +667,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
             for (int pos = 0; pos < 128; ++pos) {
               const uint32_t d = desc[rgp * 128 + pos];
               const uint32_t wd = d >> 18;
-              const float code = float(pack_min(blk, rgp * 128 + pos) + field_at(blk, (d & 0x3ffffu) + t16 * wd, wd));
+              const float code = float(pack_min(bg, rgp * 128 + pos) + field_at(bg, (d & 0x3ffffu) + t16 * wd, wd));
               const float qc = qu[g * kD + kpos_to_col(pos, kD)];
               acc = fmaf(code, qc, acc);
               qsum += qc;
@@ -803,11 +826,11 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
     load_w(k + 1, cn);
     cs = cn;
     const uint8_t* gblk;
-    const uint8_t* sblk = F.wait(k, &gblk);
+    const uint32_t sblk = F.wait(k, &gblk);
     // one block: B operand, then the IMMA fast path or the scalar path.  Called
     // with the shared-memory copy (LDS), or for a block too large to stage with
     // the global-memory block (generic loads, scalar path only).
-    auto process = [&](const uint8_t* blk, bool may_fast) {
+    auto process = [&](auto blk, bool may_fast) {
       Chunk ch;
       const bool fast = parse_chunk(blk, lane, ch) && may_fast;
       // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits, f a power of two
@@ -816,7 +839,7 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
       float mx = 0.f;
 #pragma unroll
       for (int e2 = 0; e2 < TPL / 2; ++e2) {
-        const uint2 pr = *(const uint2*)(blk + kPar + 4 * (wt0 + 2 * e2));
+        const uint2 pr = ld64(blk + kPar + 4 * (wt0 + 2 * e2));
         const float s0 = h2f(pr.x & 0xffff), s1 = h2f(pr.y & 0xffff);
         zacc = fmaf(wc[2 * e2], h2f(pr.x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr.y >> 16), zacc));
         xs[2 * e2] = wc[2 * e2] * s0;
@@ -857,13 +880,12 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
         // lane (gi, tq) = chunk 8tq + gi of the scan
         const int src = 8 * tq + gi;
         uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src);
-        const uint2 nb = *(const uint2*)(blk + kNib + 8 * src);
+        const uint2 nb = ld64(blk + kNib + 8 * src);
         uint32_t mn[8];
         {
-          const uint2* mp = (const uint2*)(blk + kMin + 32 * src);
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            const uint2 v = mp[q4];
+            const uint2 v = ld64(blk + kMin + 32 * src + 8 * q4);
             mn[2 * q4] = v.x;
             mn[2 * q4 + 1] = v.y;
           }
@@ -924,7 +946,7 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
           for (int q4 = 0; q4 < 4; ++q4) sacc[g][q4] = vsl[g * kD + lane + 32 * q4];
 #pragma unroll 1
         for (int r = 0; r < kRows; ++r) {
-          const uint32_t pr = *(const uint32_t*)(blk + kPar + 4 * r);
+          const uint32_t pr = ld32(gptr(blk) + kPar + 4 * r);
           const float s = h2f(pr & 0xffff);
           float ws[8];
 #pragma unroll
@@ -935,7 +957,7 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
             const int c = lane + 32 * q4;
             const uint32_t dd = desc[rgp * 128 + c];
             const uint32_t wd = dd >> 18;
-            const float code = float(pack_min(blk, rgp * 128 + c) + field_at(blk, (dd & 0x3ffffu) + tt * wd, wd));
+            const float code = float(pack_min(gptr(blk), rgp * 128 + c) + field_at(gptr(blk), (dd & 0x3ffffu) + tt * wd, wd));
 #pragma unroll
             for (int g = 0; g < 8; ++g) sacc[g][q4] = fmaf(ws[g], code, sacc[g][q4]);
           }
@@ -951,7 +973,7 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
       if (gblk)
         process(gblk, false);
       else
-        process(sblk, true);
+        process(F.ring + (sblk - smem_u32(F.ring)), true);  // a pointer into the ring: the compiler emits LDS
     }
     F.refill(L, 1, NB, rg, nk, k, F.tail_after(k), lane);
   }
