@@ -981,14 +981,17 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
 }
 
 // out[b][h*G+g][c] = sum over the warps whose range meets unit u (ascending) of
-// their partials (channels and z term), plus the residue rows.  One CTA per
-// (unit, head): thread c < 128 owns channel c.
-__global__ void __launch_bounds__(128) fused_v_fast_finalize(pkv_layer_t L, const float* __restrict__ part,
+// their partials (channels and z term), plus the residue rows.  One CTA of 512
+// threads per (unit, head): thread (q, c) sums slots q, q+4, ... of channel c
+// (eight loads in flight), then the four quarter sums are added in a fixed
+// order (deterministic).
+__global__ void __launch_bounds__(512) fused_v_fast_finalize(pkv_layer_t L, const float* __restrict__ part,
                                                               const float* __restrict__ w, int G, int64_t wstride,
                                                               int NB, int64_t total, int64_t nwarps, int maxseg,
                                                               float* __restrict__ out) {
+  __shared__ float red[4][kD + 1];
   const int U = L.batch * L.heads;
-  const int c = threadIdx.x;
+  const int c = threadIdx.x & 127, qq = threadIdx.x >> 7;
   for (int ug = blockIdx.x; ug < U * G; ug += gridDim.x) {
     const int u = ug / G, g = ug - u * G;
     float s = 0.f, z = 0.f;
@@ -997,36 +1000,43 @@ __global__ void __launch_bounds__(128) fused_v_fast_finalize(pkv_layer_t L, cons
       const int ns = int(w1 - w0 + 1);
       const float* pp = part + (int64_t(u) * maxseg * G + g) * kPart;
       const int64_t st = int64_t(G) * kPart;
-      // 8 independent partial sums (loads in flight), combined in a fixed order
-      float a[8], b[8];
+      float a[8], bz[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = b[i] = 0.f;
-      int sl = 0;
-      for (; sl + 8 <= ns; sl += 8) {
+      for (int i = 0; i < 8; ++i) a[i] = bz[i] = 0.f;
+      int sl = qq;
+      for (; sl + 28 < ns; sl += 32) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          a[i] += pp[(sl + i) * st + c];
-          b[i] += pp[(sl + i) * st + kD];
+          a[i] += pp[(sl + 4 * i) * st + c];
+          bz[i] += pp[(sl + 4 * i) * st + kD];
         }
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (sl + i < ns) {
-          a[i] += pp[(sl + i) * st + c];
-          b[i] += pp[(sl + i) * st + kD];
+        if (sl + 4 * i < ns) {
+          a[i] += pp[(sl + 4 * i) * st + c];
+          bz[i] += pp[(sl + 4 * i) * st + kD];
         }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         s += a[i];
-        z += b[i];
+        z += bz[i];
       }
     }
-    const int b = u / L.heads;
-    const int nr = L.nres[b];
-    const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
-    const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
-    for (int t = 0; t < nr; ++t) s = fmaf(wr[t], __half2float(__ushort_as_half(vr[t * kD + c])), s);
-    out[int64_t(ug) * kD + c] = s + z;
+    red[qq][c] = s;
+    if (c == 0) red[qq][kD] = z;
+    __syncthreads();
+    if (qq == 0) {
+      s = ((red[0][c] + red[1][c]) + red[2][c]) + red[3][c];
+      z = ((red[0][kD] + red[1][kD]) + red[2][kD]) + red[3][kD];
+      const int b = u / L.heads;
+      const int nr = L.nres[b];
+      const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
+      const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
+      for (int t = 0; t < nr; ++t) s = fmaf(wr[t], __half2float(__ushort_as_half(vr[t * kD + c])), s);
+      out[int64_t(ug) * kD + c] = s + z;
+    }
+    __syncthreads();
   }
 }
 
@@ -1118,7 +1128,7 @@ int pkv_fast_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, i
       fused_v_fast_kernel<2><<<grid, kWV * 32, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
   }
   const int ug = L->batch * L->heads * G;
-  fused_v_fast_finalize<<<ug < 148 * 16 ? ug : 148 * 16, 128, 0, s>>>(*L, part, w, G, wstride, NB, total, nwarps, maxseg,
-                                                                        out);
+  fused_v_fast_finalize<<<ug < 148 * 4 ? ug : 148 * 4, 512, 0, s>>>(*L, part, w, G, wstride, NB, total, nwarps, maxseg,
+                                                                      out);
   return pkv_cuda_status(cudaGetLastError(), "pkv_fused_v_output(fast)");
 }

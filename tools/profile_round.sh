@@ -3,11 +3,12 @@
 # Outputs land in gpurun_out/ (summarised into profiles/ by tools/summarise_profiles.py here).
 set -x
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" --nvtx-include "cublas/" \
+    --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/launches_bench.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:i8_kernel -s 4 -c 2 -o gpurun_out/prof_full \
+ncu --set full --clock-control none --import-source on -k regex:fast_kernel -s 4 -c 2 -o gpurun_out/prof_full \
     python bench.py --steps 1 --warmup 3 --no-cublas --no-cpu-baseline > gpurun_out/prof_full.log 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    -k regex:i8_kernel -s 4 -c 2 --csv --log-file gpurun_out/traffic.csv \
+    -k regex:fast_kernel -s 4 -c 2 --csv --log-file gpurun_out/traffic.csv \
     python bench.py --steps 1 --warmup 3 --no-cublas --no-cpu-baseline > /dev/null 2>&1
 echo done

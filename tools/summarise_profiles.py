@@ -27,15 +27,19 @@ def launches(tag):
     path = os.path.join(OUT, "launches.csv")
     if not os.path.exists(path):
         return None
-    rows = [r for r in csv.reader(open(path)) if r and r[0].isdigit()]
+    allrows = [r for r in csv.reader(open(path)) if r]
+    hdr = next(r for r in allrows if r[0] == "ID")
+    ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    rows = [r for r in allrows if r[0].isdigit()]
     per = defaultdict(list)
     for r in rows:
-        if r[12] == "gpu__time_duration.sum":
-            per[short(r[4])].append(float(r[14]))
+        if r[im] == "gpu__time_duration.sum":
+            per[short(r[ik])].append(float(r[iv].replace(",", "")))
     tot = sum(sum(v) for v in per.values())
     lines = [f"# ncu launch list ({tag}): per-kernel device time, cold-cache and serialised",
-             "", "Command: `ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'i8|gemm|gemv|softmax' "
-             "python bench.py --steps 2 --warmup 3 --no-cpu-baseline`", "",
+             "", "Command: `ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include timed/ "
+             "--nvtx-include cublas/ python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (the 2 timed steps: "
+             "fused K, fused V + finalize; and the cuBLAS fp16 GEMV comparison leg)", "",
              "| kernel | launches | mean us | share of listed time |", "|---|---|---|---|"]
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1e3:.2f} | {sum(v) / tot * 100:.1f}% |")
@@ -58,7 +62,7 @@ def full(tag):
             "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active"]
     stalls = [i for i, x in enumerate(h) if "smsp__average_warps_issue_stalled" in x and "per_issue_active" in x]
     lines = [f"# ncu --set full summary ({tag})", "",
-             "Command: `ncu --set full --clock-control none --import-source on -k regex:i8_kernel -s 4 -c 2 "
+             "Command: `ncu --set full --clock-control none --import-source on -k regex:fast_kernel -s 4 -c 2 "
              "python bench.py --steps 1 --warmup 3 --no-cublas --no-cpu-baseline` (config B, one K and one V launch)", ""]
     traffic = {}
     for r in rows[2:]:
@@ -106,10 +110,14 @@ def full(tag):
     tpath = os.path.join(OUT, "traffic.csv")
     per = {}
     if os.path.exists(tpath):
-        rows = [r for r in csv.reader(open(tpath)) if r and r[0].isdigit()]
-        for r in rows:
-            kind = "k" if "fused_k" in r[4] else "v"
-            per.setdefault(kind, {})[r[12]] = float(r[14])
+        allrows = [r for r in csv.reader(open(tpath)) if r]
+        hdr = next(r for r in allrows if r[0] == "ID")
+        ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+        for r in allrows:
+            if not r[0].isdigit():
+                continue
+            kind = "k" if "fused_k" in r[ik] else "v"
+            per.setdefault(kind, {})[r[im]] = float(r[iv].replace(",", ""))
     js = {}
     for kind, m in per.items():
         js[f"B_{kind}"] = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
