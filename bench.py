@@ -388,8 +388,9 @@ def main():
                          "traffic": traffic, "algorithmic_bytes_per_launch": alg},
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": B * Hq * D * 4,
                     "d2h_bytes_per_step": world * B * Hq * D * 4,
-                    "path": "sharding.ShardedDecoder.step (public API): H2D q shard, fused K, softmax, fused V, "
-                            "NCCL all-gather of per-head outputs, D2H out",
+                    "path": "sharding.ShardedDecoder.step (public API): H2D q shard, one CUDA-graph replay of "
+                            "fused K + softmax + fused V (attention_sim.GraphedAttention), NCCL all-gather of "
+                            "per-head outputs, D2H out",
                     "ms_per_step": round(e2e_ms, 5)},
             "gpu_launches": 3 * K,
             "clocks": sampler.summary(),

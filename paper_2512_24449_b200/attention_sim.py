@@ -16,10 +16,51 @@ from .kv_store import CompressedStore
 
 
 def attention_decode_batched(store: CompressedStore, layer: int, q) -> torch.Tensor:
-    """q [B, Hq, D] -> out [B, Hq, D]."""
+    """q [B, Hq, D] -> out [B, Hq, D].  The 1/sqrt(d) scale is applied to the
+    (small) query instead of the [B, Hq, L] scores: scores are linear in q
+    (SPEC.md:484), so this saves a full pass over the score tensor."""
+    q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
     s = fused_k_scores_batched(store, layer, q)
-    a = torch.softmax(s * (1.0 / math.sqrt(store.head_dim)), dim=-1)
+    a = torch.softmax(s, dim=-1)
     return fused_v_output_batched(store, layer, a)
+
+
+class GraphedAttention:
+    """attention_decode_batched for one layer, captured into a CUDA graph and
+    replayed: a decode step is then one graph launch (fused K, softmax, fused V
+    + finalize) instead of a dozen host-driven launches.  The graph is
+    re-captured whenever the layer's block / residue counts or its device
+    buffers change (every 64 appended tokens, or when the store grows)."""
+
+    def __init__(self, store: CompressedStore, layer: int):
+        self.store, self.layer = store, layer
+        self._key = None
+        self._graph = None
+        self._q = None
+        self._out = None
+
+    def _state(self, q: torch.Tensor):
+        ls = self.store[self.layer]
+        return (ls.nblk_h, ls.nres_h, ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(),
+                tuple(q.shape), q.device)
+
+    def __call__(self, q: torch.Tensor) -> torch.Tensor:
+        q = _as_f32(q, self.store.device)
+        key = self._state(q)
+        if key != self._key:
+            self._q = q.clone()
+            side = torch.cuda.Stream(device=q.device)
+            side.wait_stream(torch.cuda.current_stream(q.device))
+            with torch.cuda.stream(side):  # warm-up outside capture (scratch, occupancy queries)
+                attention_decode_batched(self.store, self.layer, self._q)
+            torch.cuda.current_stream(q.device).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._out = attention_decode_batched(self.store, self.layer, self._q)
+            self._graph, self._key = g, key
+        self._q.copy_(q, non_blocking=True)
+        self._graph.replay()
+        return self._out
 
 
 def attention_decode(store: CompressedStore, layer: int, head: int, q) -> torch.Tensor:

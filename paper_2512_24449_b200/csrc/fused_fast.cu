@@ -711,12 +711,18 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
 // them in a fixed order (deterministic) plus the residue.
 constexpr int kPart = kD + 4;  // 128 channels, the z term, padding (16-byte rows)
 constexpr int kWV = 4;
-constexpr int kRBV = 10 * 1024, kNSV = 3;
+#ifndef PKV_RBV
+#define PKV_RBV 10
+#endif
+#ifndef PKV_VMIN
+#define PKV_VMIN 4
+#endif
+constexpr int kRBV = PKV_RBV * 1024, kNSV = 3;
 using FeedV = Feed<kRBV, kNSV>;
 constexpr size_t kWarpSmemV = (2048 + FeedV::bytes() + 127) / 128 * 128;
 
 template <int NT>  // n-tiles: 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
+__global__ void __launch_bounds__(kWV * 32, PKV_VMIN) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
                                                                  int64_t wstride, float* __restrict__ part, int NB,
                                                                  int64_t total, int maxseg,
                                                                  float* __restrict__ vscr) {

@@ -120,6 +120,10 @@ def make_local_store(p: Partition, layers: int, head_dim: int, **kw):
     return CompressedStore(layers, p.local_heads, head_dim, batch=p.local_batch, **kw)
 
 
-def cuda_local_attention(store, layer: int = 0):
-    from .attention_sim import attention_decode_batched
+def cuda_local_attention(store, layer: int = 0, graph: bool = True):
+    """This rank's decode attention on the CUDA path: replayed as one CUDA graph
+    per step (attention_sim.GraphedAttention) or launched eagerly."""
+    from .attention_sim import GraphedAttention, attention_decode_batched
+    if graph:
+        return GraphedAttention(store, layer)
     return lambda q_local: attention_decode_batched(store, layer, q_local)

@@ -345,3 +345,27 @@ def test_fused_default_format_paths(rels, G):
     for hq in range(H * G):
         _close(s[0, hq], O.naive_k_scores(ref, 0, hq // G, q[0, hq]))
         _close(o[0, hq], O.naive_v_output(ref, 0, hq // G, w[0, hq]))
+
+
+def test_graphed_attention_matches_eager_and_recaptures():
+    """attention_sim.GraphedAttention (one CUDA-graph launch per decode step)
+    is bit-identical to the eager composition and re-captures after appends
+    change the block / residue counts."""
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import GraphedAttention, attention_decode_batched
+    rng = np.random.default_rng(21)
+    B, H, D, G = 2, 2, 128, 4
+    st = CS(1, H, D, batch=B)
+    k = (rng.standard_normal((B, 200, H, D))).astype(np.float16)
+    v = (rng.standard_normal((B, 200, H, D))).astype(np.float16)
+    st.compress_batch(0, k, v)
+    ga = GraphedAttention(st, 0)
+    for step in range(3):
+        q = torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32)).cuda()
+        a = ga(q).clone()
+        e = attention_decode_batched(st, 0, q)
+        assert torch.equal(a, e)
+        kn = rng.standard_normal((B, 40, H, D)).astype(np.float16)
+        vn = rng.standard_normal((B, 40, H, D)).astype(np.float16)
+        st.compress_batch(0, kn, vn)  # 200 -> 240 -> 280: residue and block counts change
+    torch.cuda.synchronize()
