@@ -130,6 +130,7 @@ __device__ __forceinline__ uint32_t shf_r_clamp(uint32_t lo, uint32_t hi, uint32
 // slot's mbarrier wait, so they cannot be scheduled before it.
 __device__ __forceinline__ uint32_t ld32(const uint8_t* p) { return *(const uint32_t*)p; }
 __device__ __forceinline__ uint2 ld64(const uint8_t* p) { return *(const uint2*)p; }
+__device__ __forceinline__ uint4 ld128(const uint8_t* p) { return *(const uint4*)p; }
 __device__ __forceinline__ uint32_t ld32(uint32_t a) {
   uint32_t v;
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -192,7 +193,9 @@ __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ l
   PackLd r;
   r.w0 = ld32(p);
   r.w1 = ld32(p + 4);
-  r.w2 = ld32(p + 8);
+  // the payload (16w bits from bit % 32 in {0, 16}) needs a third word only
+  // for w = 4 starting mid-word; other lanes skip the load (no bank traffic)
+  r.w2 = (w16 == 64u && (bit & 16u)) ? ld32(p + 8) : 0u;
   r.c = *(const uint4*)(lut + w16);
   return r;
 }
@@ -230,8 +233,8 @@ __device__ __forceinline__ uint32_t pack_min(const uint8_t* __restrict__ blk, in
 }
 
 // ---------------------------------------------------------------- block parse
-// Lane `chunk` reads the width nibbles of physical packs 16*chunk .. +15 and its
-// 16 minima.  Returns the lane's starting payload bit (warp scan over chunks in
+// Lane `chunk` reads the width nibbles of physical packs 16*chunk .. +15 and the
+// 16 minima of chunk `mchunk` (its own, or the chunk it will decode).  Returns the lane's starting payload bit (warp scan over chunks in
 // lane order) and whether every pack of the block fits the fast path
 // (w <= 4 and minimum <= 240, so min + 15 fits a byte).
 struct Chunk {
@@ -240,16 +243,17 @@ struct Chunk {
   uint32_t bit;   // payload bit offset of the chunk's first pack
 };
 template <class P>
-__device__ __forceinline__ bool parse_chunk(P blk, int lane, Chunk& ch) {
+__device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& ch) {
   ch.nb = ld64(blk + kNib + 8 * lane);
+  // minima of chunk `mchunk` (32 bytes at kMin + 32*mchunk = 264 + 32*mchunk):
+  // three aligned 16-byte loads from 256 + 32*mchunk, words 2..9
+  const uint4 m0 = ld128(blk + kMin - 8 + 32 * mchunk), m1 = ld128(blk + kMin + 8 + 32 * mchunk),
+              m2 = ld128(blk + kMin + 24 + 32 * mchunk);
+  ch.mn[0] = m0.z; ch.mn[1] = m0.w; ch.mn[2] = m1.x; ch.mn[3] = m1.y;
+  ch.mn[4] = m1.z; ch.mn[5] = m1.w; ch.mn[6] = m2.x; ch.mn[7] = m2.y;
   uint32_t mor = 0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint2 v = ld64(blk + kMin + 32 * lane + 8 * q);
-    ch.mn[2 * q] = v.x;
-    ch.mn[2 * q + 1] = v.y;
-    mor |= v.x | v.y;
-  }
+  for (int q = 0; q < 8; ++q) mor |= ch.mn[q];
   const uint32_t nx = ch.nb.x, ny = ch.nb.y;
   const uint32_t bad = ((nx | ny) & 0x88888888u) |
                        (((nx >> 2) & (nx | (nx >> 1))) & 0x11111111u) | (((ny >> 2) & (ny | (ny >> 1))) & 0x11111111u);
@@ -435,6 +439,12 @@ struct Feed {
 // phase of the ldmatrix hit 8 distinct chunks, i.e. no bank conflicts).
 constexpr int kTile = 4 * 128 * 16;  // 8 KB
 constexpr int kWK = 4;               // warps per CTA
+#ifndef PKV_KQUAD
+#define PKV_KQUAD 0
+#endif
+#ifndef PKV_KMIN
+#define PKV_KMIN 1
+#endif
 #ifndef PKV_RBK
 #define PKV_RBK 10
 #endif
@@ -523,7 +533,7 @@ __device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G,
 
 
 template <int NU>  // unsigned query digit tiles: 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
+__global__ void __launch_bounds__(kWK * 32, PKV_KMIN) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
                                                                  float* __restrict__ scores, int64_t sstride, int NB,
                                                                  int64_t total) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -568,8 +578,37 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
     const uint32_t blk = F.wait(k, &gblk);
     if (j < nbk) {
       Chunk ch;
-      const bool fast = gblk == nullptr && parse_chunk(blk, lane, ch);
+      const bool fast = gblk == nullptr && parse_chunk(blk, lane, lane, ch);
       if (fast) {
+#if PKV_KQUAD
+        // packs in quads (four independent decode chains), loads one quad ahead
+        uint32_t bits[17];
+        bits[0] = ch.bit;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) bits[i + 1] = bits[i] + w16_of(ch.nb, i);
+        PackLd Lq[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Lq[e] = pack_load(blk, lutb, bits[e], bits[e + 1] - bits[e]);
+#pragma unroll
+        for (int i4 = 0; i4 < 16; i4 += 4) {
+          PackLd Nq[4];
+          if (i4 < 12) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) Nq[e] = pack_load(blk, lutb, bits[i4 + 4 + e], bits[i4 + 5 + e] - bits[i4 + 4 + e]);
+          }
+          uint32_t rq[4][4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pack_decode(Lq[e], bits[i4 + e], min_rep(ch.mn, i4 + e), rq[e]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            *(uint4*)(tile + ((e & 1) ? st_odd : st_even) + 128u * ((i4 + e) >> 1)) =
+                make_uint4(rq[e][0], rq[e][1], rq[e][2], rq[e][3]);
+          if (i4 < 12) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) Lq[e] = Nq[e];
+          }
+        }
+#else
         // packs in pairs (two independent decode chains), loads one pair ahead
         uint32_t bit = ch.bit;
         uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
@@ -599,6 +638,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
             B = nB;
           }
         }
+#endif
         // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
         uint32_t prm[4][2];
 #pragma unroll
@@ -653,7 +693,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
         float* srow = sbase + j * kRows;
         uint32_t* desc = (uint32_t*)tile;
         const uint8_t* bg = gblk ? gblk : gptr(blk);
-        if (gblk) parse_chunk(bg, lane, ch);
+        if (gblk) parse_chunk(bg, lane, lane, ch);
         build_desc(ch, lane, desc);
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
@@ -838,7 +878,8 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMIN) fused_v_fast_kernel(pkv_la
     // the global-memory block (generic loads, scalar path only).
     auto process = [&](auto blk, bool may_fast) {
       Chunk ch;
-      const bool fast = parse_chunk(blk, lane, ch) && may_fast;
+      const int src = 8 * tq + gi;  // the chunk this lane decodes (row-group tq, channels 16gi..)
+      const bool fast = parse_chunk(blk, lane, src, ch) && may_fast;
       // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits, f a power of two
       // per (block, head) with max x * f < 2^16; z term sum_t w_t z_t in f32
       float xs[TPL];
@@ -883,19 +924,10 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMIN) fused_v_fast_kernel(pkv_la
       }
       __syncwarp();  // frag reads done (the slow path reuses the area)
       if (fast) {
-        // lane (gi, tq) = chunk 8tq + gi of the scan
-        const int src = 8 * tq + gi;
+        // lane (gi, tq) = chunk 8tq + gi of the scan (its minima are in ch.mn)
         uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src);
         const uint2 nb = ld64(blk + kNib + 8 * src);
-        uint32_t mn[8];
-        {
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const uint2 v = ld64(blk + kMin + 32 * src + 8 * q4);
-            mn[2 * q4] = v.x;
-            mn[2 * q4 + 1] = v.y;
-          }
-        }
+        const uint32_t (&mn)[8] = ch.mn;
         // the m-tile's two packs decoded together, the next pair's loads in flight
         uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
         PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
