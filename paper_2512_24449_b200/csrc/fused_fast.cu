@@ -196,7 +196,7 @@ __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ l
   // the payload (16w bits from bit % 32 in {0, 16}) needs a third word only
   // for w = 4 starting mid-word; other lanes skip the load (no bank traffic)
   r.w2 = (w16 == 64u && (bit & 16u)) ? ld32(p + 8) : 0u;
-  r.c = *(const uint4*)(lut + w16);
+  r.c = *(const uint4*)(lut + w16);  // (computing the constants instead measured slower)
   return r;
 }
 // r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
@@ -439,16 +439,7 @@ struct Feed {
 // phase of the ldmatrix hit 8 distinct chunks, i.e. no bank conflicts).
 constexpr int kTile = 4 * 128 * 16;  // 8 KB
 constexpr int kWK = 4;               // warps per CTA
-#ifndef PKV_KQUAD
-#define PKV_KQUAD 0
-#endif
-#ifndef PKV_KMIN
-#define PKV_KMIN 1
-#endif
-#ifndef PKV_RBK
-#define PKV_RBK 10
-#endif
-constexpr int kRBK = PKV_RBK * 1024, kNSK = 3;
+constexpr int kRBK = 10 * 1024, kNSK = 3;
 using FeedK = Feed<kRBK, kNSK>;
 constexpr size_t kWarpSmemK = (kTile + FeedK::bytes() + 127) / 128 * 128;
 
@@ -533,7 +524,7 @@ __device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G,
 
 
 template <int NU>  // unsigned query digit tiles: 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kWK * 32, PKV_KMIN) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
+__global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
                                                                  float* __restrict__ scores, int64_t sstride, int NB,
                                                                  int64_t total) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -580,35 +571,6 @@ __global__ void __launch_bounds__(kWK * 32, PKV_KMIN) fused_k_fast_kernel(pkv_la
       Chunk ch;
       const bool fast = gblk == nullptr && parse_chunk(blk, lane, lane, ch);
       if (fast) {
-#if PKV_KQUAD
-        // packs in quads (four independent decode chains), loads one quad ahead
-        uint32_t bits[17];
-        bits[0] = ch.bit;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) bits[i + 1] = bits[i] + w16_of(ch.nb, i);
-        PackLd Lq[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) Lq[e] = pack_load(blk, lutb, bits[e], bits[e + 1] - bits[e]);
-#pragma unroll
-        for (int i4 = 0; i4 < 16; i4 += 4) {
-          PackLd Nq[4];
-          if (i4 < 12) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) Nq[e] = pack_load(blk, lutb, bits[i4 + 4 + e], bits[i4 + 5 + e] - bits[i4 + 4 + e]);
-          }
-          uint32_t rq[4][4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pack_decode(Lq[e], bits[i4 + e], min_rep(ch.mn, i4 + e), rq[e]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            *(uint4*)(tile + ((e & 1) ? st_odd : st_even) + 128u * ((i4 + e) >> 1)) =
-                make_uint4(rq[e][0], rq[e][1], rq[e][2], rq[e][3]);
-          if (i4 < 12) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) Lq[e] = Nq[e];
-          }
-        }
-#else
         // packs in pairs (two independent decode chains), loads one pair ahead
         uint32_t bit = ch.bit;
         uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
@@ -638,7 +600,6 @@ __global__ void __launch_bounds__(kWK * 32, PKV_KMIN) fused_k_fast_kernel(pkv_la
             B = nB;
           }
         }
-#endif
         // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
         uint32_t prm[4][2];
 #pragma unroll
@@ -751,18 +712,12 @@ __global__ void __launch_bounds__(kWK * 32, PKV_KMIN) fused_k_fast_kernel(pkv_la
 // them in a fixed order (deterministic) plus the residue.
 constexpr int kPart = kD + 4;  // 128 channels, the z term, padding (16-byte rows)
 constexpr int kWV = 4;
-#ifndef PKV_RBV
-#define PKV_RBV 10
-#endif
-#ifndef PKV_VMIN
-#define PKV_VMIN 4
-#endif
-constexpr int kRBV = PKV_RBV * 1024, kNSV = 3;
+constexpr int kRBV = 10 * 1024, kNSV = 3;
 using FeedV = Feed<kRBV, kNSV>;
 constexpr size_t kWarpSmemV = (2048 + FeedV::bytes() + 127) / 128 * 128;
 
 template <int NT>  // n-tiles: 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kWV * 32, PKV_VMIN) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
+__global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
                                                                  int64_t wstride, float* __restrict__ part, int NB,
                                                                  int64_t total, int maxseg,
                                                                  float* __restrict__ vscr) {
