@@ -154,6 +154,18 @@ int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const float* w, in
                        int64_t w_stride, float* out, void* scratch, int64_t scratch_bytes,
                        void* stream);
 
+/* --- decode attention (SPEC.md:520-528 attention_decode) ----------------- */
+/* Scratch bytes for pkv_attention_decode (0: format not fused, -1: bad args). */
+int64_t pkv_attention_scratch_bytes(const pkv_layer_t* L, int32_t nblocks, int32_t q_heads);
+/* out[b][hq] = softmax(scores[b][hq]) . deq(V[b, hq/G]) with
+ * scores = deq(K)·q written to `scores` ([B][q_heads][score_stride] f32, the
+ * caller pre-scales q by 1/sqrt(d)).  Three launches: fused K (also records
+ * per-slot score maxima), fused V on exp(s - M) with the row maximum M (no
+ * softmax pass, no rescaling), normalising finalize.  Default format only
+ * (pack 16, head_dim 128, block 64, G <= 8); else PKV_E_ARG.            */
+int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const float* q, int32_t q_heads, float* scores,
+                         int64_t score_stride, float* out, void* scratch, int64_t scratch_bytes, void* stream);
+
 /* --- parity / debug ------------------------------------------------------ */
 /* Decodes every block of one kind into codes [B*H][max_blocks][block][D]
  * (block-row order) and params [B*H][max_blocks][block][2] f32.            */

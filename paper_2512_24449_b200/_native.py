@@ -61,6 +61,9 @@ _SIGS = {
     "pkv_fused_v_output": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_int64,
                                      c_void_p]),
     "pkv_decode_store": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_void_p, c_void_p]),
+    "pkv_attention_scratch_bytes": (c_int64, [POINTER(Layer), c_int32, c_int32]),
+    "pkv_attention_decode": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p,
+                                       c_int64, c_void_p]),
 }
 
 _lib = None

@@ -10,16 +10,43 @@ import math
 
 import torch
 
+from . import _native as N
 from . import errors as E
 from .fused_kernels import fused_k_scores_batched, fused_v_output_batched, _as_f32
-from .kv_store import CompressedStore
+from .kv_store import CompressedStore, ctypes_ref
 
 
 def attention_decode_batched(store: CompressedStore, layer: int, q) -> torch.Tensor:
-    """q [B, Hq, D] -> out [B, Hq, D].  The 1/sqrt(d) scale is applied to the
-    (small) query instead of the [B, Hq, L] scores: scores are linear in q
-    (SPEC.md:484), so this saves a full pass over the score tensor."""
+    """q [B, Hq, D] -> out [B, Hq, D].
+
+    The 1/sqrt(d) scale is applied to the (small) query instead of the
+    [B, Hq, L] scores (scores are linear in q).  For the default
+    format the softmax is folded into the fused kernels (pkv_attention_decode:
+    the K launch records per-slot score maxima, the V launch weights rows with
+    exp(s - max) and the finalize divides by the sum), so the scores are
+    written once and read once; other formats compose fused K -> softmax ->
+    fused V."""
     q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
+    ls = store[layer]
+    B, H, D = store.batch, store.heads, store.head_dim
+    if q.dim() != 3 or q.shape[0] != B or q.shape[2] != D or q.shape[1] % H:
+        raise E.ShapeMismatchError(f"q must be [B={B}, Hq (multiple of {H}), D={D}], got {tuple(q.shape)}")
+    Hq = int(q.shape[1])
+    lib = N.lib()
+    st = ls.struct()
+    need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(st), ls.nblk_h, Hq))
+    if need > 0:
+        L = ls.tokens
+        stride = max(L, 1)
+        stride = (stride + 3) // 4 * 4
+        scores = torch.empty((B, Hq, stride), dtype=torch.float32, device=store.device)
+        out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
+        if ls.a_scratch.numel() < need:
+            ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=store.device)
+        N.check(lib.pkv_attention_decode(ctypes_ref(st), ls.nblk_h, N.ptr(q), Hq, N.ptr(scores), stride, N.ptr(out),
+                                         N.ptr(ls.a_scratch), int(ls.a_scratch.numel()), N.stream()),
+                "attention_decode")
+        return out
     s = fused_k_scores_batched(store, layer, q)
     a = torch.softmax(s, dim=-1)
     return fused_v_output_batched(store, layer, a)

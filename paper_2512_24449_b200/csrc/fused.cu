@@ -30,6 +30,9 @@ int pkv_fast_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, f
 int pkv_fast_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
                      float* part, cudaStream_t s);
 int64_t pkv_fast_v_scratch(const pkv_layer_t* L, int nblocks, int G);
+int64_t pkv_fast_attention_scratch(const pkv_layer_t* L, int nblocks, int G);
+int pkv_fast_attention(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
+                       float* out, float* scratch, cudaStream_t s);
 
 namespace {
 
@@ -406,4 +409,33 @@ extern "C" int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const f
                     return (launch_v<KPc, Dc, 16>(L, nblocks, w, G, w_stride, out, part, strm)));
   }
   return PKV_OK;
+}
+
+extern "C" int64_t pkv_attention_scratch_bytes(const pkv_layer_t* L, int32_t nblocks, int32_t q_heads) {
+  int G = 0;
+  if (fused_args(L, nblocks, q_heads, &G)) return -1;
+  if (!pkv_fast_supported(L, G, 4)) return 0;
+  return pkv_fast_attention_scratch(L, nblocks, G);
+}
+
+extern "C" int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const float* q, int32_t q_heads,
+                                    float* scores, int64_t score_stride, float* out, void* scratch,
+                                    int64_t scratch_bytes, void* stream) {
+  int G = 0;
+  int s = fused_args(L, nblocks, q_heads, &G);
+  if (s) return s;
+  if (!pkv_fast_supported(L, G, score_stride) || (reinterpret_cast<uintptr_t>(q) & 15) ||
+      (reinterpret_cast<uintptr_t>(scores) & 15)) {
+    pkv_set_error("attention_decode: only the default format (pack 16, head_dim 128, block 64, G <= 8) is fused");
+    return PKV_E_ARG;
+  }
+  if (score_stride < int64_t(nblocks) * 64 + L->buffer && score_stride < int64_t(nblocks) * 64) {
+    pkv_set_error("score_stride too small");
+    return PKV_E_SHAPE;
+  }
+  if (scratch_bytes < pkv_fast_attention_scratch(L, nblocks, G)) {
+    pkv_set_error("attention scratch too small");
+    return PKV_E_ARG;
+  }
+  return pkv_fast_attention(L, nblocks, q, G, scores, score_stride, out, (float*)scratch, (cudaStream_t)stream);
 }

@@ -443,6 +443,11 @@ constexpr int kRBK = 10 * 1024, kNSK = 3;
 using FeedK = Feed<kRBK, kNSK>;
 constexpr size_t kWarpSmemK = (kTile + FeedK::bytes() + 127) / 128 * 128;
 
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(PKV_FULL, v, o));
+  return v;
+}
 __device__ __forceinline__ float sel8(const float (&v)[8], int i) {
   float r = v[0];
 #pragma unroll
@@ -523,10 +528,14 @@ __device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G,
 }
 
 
-template <int NU>  // unsigned query digit tiles: 1 for G <= 4, 2 for G <= 8
+// ST: also record softmax statistics for attention_decode: the maximum score of
+// every (unit, warp slot, head) in kmax[u][slot][g] and of the residue rows in
+// kres[u][g] (-inf when there are none).
+template <int NU, bool ST>  // NU: unsigned query digit tiles, 1 for G <= 4, 2 for G <= 8
 __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
                                                                  float* __restrict__ scores, int64_t sstride, int NB,
-                                                                 int64_t total) {
+                                                                 int64_t total, float* __restrict__ kmax,
+                                                                 float* __restrict__ kres, int kslots) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gi = lane >> 2, tq = lane & 3;
   const int U = L.batch * L.heads, Hq = L.heads * G;
@@ -551,6 +560,20 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   QFrag<NU> Q;
   int cur_u = -1, nbk = 0;
   float* sbase = scores;
+  float kmx0 = -INFINITY, kmx1 = -INFINITY;  // running max of this lane's scores (heads tq, tq + 4)
+  // the unit's score maxima of this warp -> kmax[u][slot][g] (lanes with gi = 0 write)
+  auto flush_max = [&](int u) {
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      kmx0 = fmaxf(kmx0, __shfl_xor_sync(PKV_FULL, kmx0, o));
+      kmx1 = fmaxf(kmx1, __shfl_xor_sync(PKV_FULL, kmx1, o));
+    }
+    const int64_t slot = wid - warp_of(int64_t(u) * NB, total, nwarps);
+    float* km = kmax + (int64_t(u) * kslots + slot) * G;
+    if (gi == 0 && tq < G) km[tq] = kmx0;
+    if (gi == 0 && tq + 4 < G) km[tq + 4] = kmx1;
+    kmx0 = kmx1 = -INFINITY;
+  };
   Cursor cs;
   cs.init(rg.b0, NB);
   F.refill(L, 0, NB, rg, nk, -1, 0u, lane);
@@ -559,6 +582,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   for (int k = 0; k < nk; ++k, cs.step(1, NB)) {
     const int u = cs.u, j = cs.j;
     if (u != cur_u) {
+      if (ST && cur_u >= 0) flush_max(cur_u);
       cur_u = u;
       const int b = u / L.heads, h = u - b * L.heads;
       nbk = L.nblk[b];
@@ -636,14 +660,18 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
           if (tq < G) {
             const float vA = fmaf(65536.f, float(accS[0]), float(accU[0][0] + 256 * accU[0][1]));
             const float vB = fmaf(65536.f, float(accS[2]), float(accU[0][2] + 256 * accU[0][3]));
-            p0[16 * g] = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]);
-            p0[16 * g + 8] = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
+            const float scA = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]), scB = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
+            p0[16 * g] = scA;
+            p0[16 * g + 8] = scB;
+            if (ST) kmx0 = fmaxf(kmx0, fmaxf(scA, scB));
           }
           if (NU == 2 && tq + 4 < G) {
             const float vA = fmaf(65536.f, float(accS[1]), float(accU[NU - 1][0] + 256 * accU[NU - 1][1]));
             const float vB = fmaf(65536.f, float(accS[3]), float(accU[NU - 1][2] + 256 * accU[NU - 1][3]));
-            p1[16 * g] = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]);
-            p1[16 * g + 8] = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
+            const float scA = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]), scB = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
+            p1[16 * g] = scA;
+            p1[16 * g + 8] = scB;
+            if (ST) kmx1 = fmaxf(kmx1, fmaxf(scA, scB));
           }
         }
         __syncwarp();  // tile reads done before the next block's stores
@@ -673,7 +701,15 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
               acc = fmaf(code, qc, acc);
               qsum += qc;
             }
-            srow[int64_t(g) * sstride + tt] = fmaf(s, acc, z * qsum);
+            const float sc = fmaf(s, acc, z * qsum);
+            srow[int64_t(g) * sstride + tt] = sc;
+            if (ST) {  // fold into the lanes that own head g's running max
+              const float m = warp_max(sc);
+              if ((g & 3) == tq) {
+                if (g < 4) kmx0 = fmaxf(kmx0, m);
+                else kmx1 = fmaxf(kmx1, m);
+              }
+            }
           }
         }
         __syncwarp();
@@ -681,6 +717,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
     }
     F.refill(L, 0, NB, rg, nk, k, F.tail_after(k), lane);
   }
+  if (ST && cur_u >= 0) flush_max(cur_u);
   // uncompressed residue rows of units u = wid, wid + nwarps, ...
   for (int64_t uu = wid; uu < U; uu += nwarps) {
     const int u = int(uu);
@@ -689,14 +726,17 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
     const uint16_t* kr = L.stage + (int64_t(0) * U + u) * L.buffer * kD;
     const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
     float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride + int64_t(L.nblk[b]) * kRows;
+    float rm = -INFINITY;  // (lane g keeps head g's residue maximum)
     for (int t = 0; t < nr; ++t) {
       for (int g = 0; g < G; ++g) {
         float a = 0.f;
         for (int c = lane; c < kD; c += 32) a = fmaf(__half2float(__ushort_as_half(kr[t * kD + c])), qu[g * kD + c], a);
         a = warp_sum(a);
         if (lane == 0) srow[int64_t(g) * sstride + t] = a;
+        if (lane == g) rm = fmaxf(rm, a);
       }
     }
+    if (ST && lane < G) kres[int64_t(u) * G + lane] = rm;
   }
 }
 
@@ -710,17 +750,37 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
 // (gi, tq) owns out[head 4nt + tq][channels 16gi .. 16gi+15].  Per (warp,
 // range segment = unit) partial sums go to scratch; the finalize kernel adds
 // them in a fixed order (deterministic) plus the residue.
-constexpr int kPart = kD + 4;  // 128 channels, the z term, padding (16-byte rows)
+constexpr int kPart = kD + 4;  // 128 channels, the z term, l (attention), padding (16-byte rows)
+
+// Row maximum of head g of unit u over the K launch's warp slots and residue
+// rows; the `nl` lanes of a group share the loads and reduce with shuffles.
+__device__ __forceinline__ float row_max(const float* __restrict__ kmax, const float* __restrict__ kres, int u, int g,
+                                         int G, int NB, int64_t ktotal, int64_t knwarps, int kslots, int sub, int nl) {
+  float m = sub == 0 ? kres[int64_t(u) * G + g] : -INFINITY;
+  if (ktotal > 0) {
+    const int64_t w0 = warp_of(int64_t(u) * NB, ktotal, knwarps), w1 = warp_of(int64_t(u + 1) * NB - 1, ktotal, knwarps);
+    for (int64_t sl = sub; sl <= w1 - w0; sl += nl) m = fmaxf(m, kmax[(int64_t(u) * kslots + sl) * G + g]);
+  }
+  for (int o = 1; o < nl; o <<= 1) m = fmaxf(m, __shfl_xor_sync(PKV_FULL, m, o));
+  return m;
+}
 constexpr int kWV = 4;
 constexpr int kRBV = 10 * 1024, kNSV = 3;
 using FeedV = Feed<kRBV, kNSV>;
 constexpr size_t kWarpSmemV = (2048 + FeedV::bytes() + 127) / 128 * 128;
 
-template <int NT>  // n-tiles: 1 for G <= 4, 2 for G <= 8
+// SM (attention_decode): `w` holds raw (scaled) scores instead of softmax
+// weights; every block uses p_t = exp(s_t - M) with M the row maximum from
+// the K launch's statistics (kmax over its kslots warp slots, kres), so no
+// rescaling is ever needed, and each partial slot also carries l = sum p.
+template <int NT, bool SM>  // NT: n-tiles, 1 for G <= 4, 2 for G <= 8
 __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
                                                                  int64_t wstride, float* __restrict__ part, int NB,
                                                                  int64_t total, int maxseg,
-                                                                 float* __restrict__ vscr) {
+                                                                 float* __restrict__ vscr,
+                                                                 const float* __restrict__ kmax,
+                                                                 const float* __restrict__ kres, int kslots,
+                                                                 int64_t knwarps, int64_t ktotal) {
   constexpr int GP = 4 * NT;    // padded heads
   constexpr int LPH = 32 / GP;  // writer lanes per head
   constexpr int TPL = 64 / LPH; // rows per writer lane (8 or 16)
@@ -748,7 +808,8 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
   const int u_last = nk > 0 ? int((rg.b1 - 1) / NB) : u_first - 1;
 
   float acc[NT][16];
-  float zacc = 0.f;
+  float zacc = 0.f, lacc = 0.f;
+  float Mh = 0.f;  // SM: row maximum (times log2 e) of the writer head wh for the current unit
   bool slow_used = false;
   int seg = 0;  // segment (unit - u_first) the accumulators belong to
 #pragma unroll
@@ -773,11 +834,17 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc[nt][i] = 0.f;
     }
-    float z = zacc;
+    float z = zacc, l = lacc;
 #pragma unroll
-    for (int o = 1; o < LPH; o <<= 1) z += __shfl_xor_sync(PKV_FULL, z, o);
-    if (lane % LPH == 0 && wh < G) pp[wh * kPart + kD] = z;
-    zacc = 0.f;
+    for (int o = 1; o < LPH; o <<= 1) {
+      z += __shfl_xor_sync(PKV_FULL, z, o);
+      if (SM) l += __shfl_xor_sync(PKV_FULL, l, o);
+    }
+    if (lane % LPH == 0 && wh < G) {
+      pp[wh * kPart + kD] = z;
+      if (SM) pp[wh * kPart + kD + 1] = l;
+    }
+    zacc = lacc = 0.f;
     if (slow_used) {
       __syncwarp();
       for (int e = lane; e < G * kD; e += 32) {
@@ -818,6 +885,7 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
       b = u / L.heads;
       h = u - b * L.heads;
       nbk = L.nblk[b];
+      if (SM) Mh = row_max(kmax, kres, u, wh < G ? wh : 0, G, NB, ktotal, knwarps, kslots, lane % LPH, LPH) * 1.4426950408889634f;
     }
     while (seg < u - u_first) flush();
     float wc[TPL];
@@ -839,6 +907,13 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
       // per (block, head) with max x * f < 2^16; z term sum_t w_t z_t in f32
       float xs[TPL];
       float mx = 0.f;
+      if (SM) {
+#pragma unroll
+        for (int e = 0; e < TPL; ++e) {
+          wc[e] = exp2f(fmaf(wc[e], 1.4426950408889634f, -Mh));  // p_t = exp(s_t - M)
+          lacc += wc[e];
+        }
+      }
 #pragma unroll
       for (int e2 = 0; e2 < TPL / 2; ++e2) {
         const uint2 pr = ld64(blk + kPar + 4 * (wt0 + 2 * e2));
@@ -932,6 +1007,9 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
           slow_used = true;
         }
         const float* wu = w + (int64_t(b) * Hq + int64_t(h) * G) * wstride + int64_t(j) * kRows;
+        float Mg[8];  // SM: every head's row maximum (from its writer lanes)
+#pragma unroll
+        for (int g = 0; g < 8; ++g) Mg[g] = __shfl_sync(PKV_FULL, Mh, (g < GP ? g : 0) * LPH);
         float sacc[8][4];
 #pragma unroll
         for (int g = 0; g < 8; ++g)
@@ -943,7 +1021,11 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
           const float s = h2f(pr & 0xffff);
           float ws[8];
 #pragma unroll
-          for (int g = 0; g < 8; ++g) ws[g] = g < G ? wu[int64_t(g) * wstride + r] * s : 0.f;
+          for (int g = 0; g < 8; ++g) {
+          float wv = g < G ? wu[int64_t(g) * wstride + r] : 0.f;
+          if (SM && g < G) wv = exp2f(fmaf(wv, 1.4426950408889634f, -Mg[g]));
+          ws[g] = wv * s;
+        }
           const int rgp = r >> 4, tt = r & 15;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -977,31 +1059,42 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
 // their partials (channels and z term), plus the residue rows.  One CTA of 512
 // threads per (unit, head): thread (q, c) sums slots q, q+4, ... of channel c
 // (eight loads in flight), then the four quarter sums are added in a fixed
-// order (deterministic).
+// order (deterministic).  SM: `w` holds scores; the result is divided by the
+// softmax denominator (sum of the slots' l plus the residue rows' weights).
+template <bool SM>
 __global__ void __launch_bounds__(512) fused_v_fast_finalize(pkv_layer_t L, const float* __restrict__ part,
                                                               const float* __restrict__ w, int G, int64_t wstride,
                                                               int NB, int64_t total, int64_t nwarps, int maxseg,
-                                                              float* __restrict__ out) {
-  __shared__ float red[4][kD + 1];
+                                                              float* __restrict__ out, const float* __restrict__ kmax,
+                                                              const float* __restrict__ kres, int kslots,
+                                                              int64_t knwarps, int64_t ktotal) {
+  __shared__ float red[4][kD + 2];
+  __shared__ float Msh;
   const int U = L.batch * L.heads;
   const int c = threadIdx.x & 127, qq = threadIdx.x >> 7;
   for (int ug = blockIdx.x; ug < U * G; ug += gridDim.x) {
     const int u = ug / G, g = ug - u * G;
-    float s = 0.f, z = 0.f;
+    if (SM && threadIdx.x < 32) {
+      const float m = row_max(kmax, kres, u, g, G, NB, ktotal, knwarps, kslots, threadIdx.x, 32);
+      if (threadIdx.x == 0) Msh = m;
+    }
+    float s = 0.f, z = 0.f, l = 0.f;
     if (total > 0 && NB > 0) {
       const int64_t w0 = warp_of(int64_t(u) * NB, total, nwarps), w1 = warp_of(int64_t(u + 1) * NB - 1, total, nwarps);
       const int ns = int(w1 - w0 + 1);
       const float* pp = part + (int64_t(u) * maxseg * G + g) * kPart;
       const int64_t st = int64_t(G) * kPart;
-      float a[8], bz[8];
+      // eight independent partial sums (loads in flight), combined in a fixed order
+      float a[8], bz[8], bl[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = bz[i] = 0.f;
+      for (int i = 0; i < 8; ++i) a[i] = bz[i] = bl[i] = 0.f;
       int sl = qq;
       for (; sl + 28 < ns; sl += 32) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           a[i] += pp[(sl + 4 * i) * st + c];
           bz[i] += pp[(sl + 4 * i) * st + kD];
+          if (SM) bl[i] += pp[(sl + 4 * i) * st + kD + 1];
         }
       }
 #pragma unroll
@@ -1009,25 +1102,36 @@ __global__ void __launch_bounds__(512) fused_v_fast_finalize(pkv_layer_t L, cons
         if (sl + 4 * i < ns) {
           a[i] += pp[(sl + 4 * i) * st + c];
           bz[i] += pp[(sl + 4 * i) * st + kD];
+          if (SM) bl[i] += pp[(sl + 4 * i) * st + kD + 1];
         }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         s += a[i];
         z += bz[i];
+        l += bl[i];
       }
     }
     red[qq][c] = s;
-    if (c == 0) red[qq][kD] = z;
+    if (c == 0) {
+      red[qq][kD] = z;
+      red[qq][kD + 1] = l;
+    }
     __syncthreads();
     if (qq == 0) {
       s = ((red[0][c] + red[1][c]) + red[2][c]) + red[3][c];
       z = ((red[0][kD] + red[1][kD]) + red[2][kD]) + red[3][kD];
+      l = ((red[0][kD + 1] + red[1][kD + 1]) + red[2][kD + 1]) + red[3][kD + 1];
       const int b = u / L.heads;
       const int nr = L.nres[b];
       const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
       const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
-      for (int t = 0; t < nr; ++t) s = fmaf(wr[t], __half2float(__ushort_as_half(vr[t * kD + c])), s);
-      out[int64_t(ug) * kD + c] = s + z;
+      const float M = SM ? Msh : 0.f;
+      for (int t = 0; t < nr; ++t) {
+        const float p = SM ? expf(wr[t] - M) : wr[t];
+        s = fmaf(p, __half2float(__ushort_as_half(vr[t * kD + c])), s);
+        l += p;
+      }
+      out[int64_t(ug) * kD + c] = SM ? (s + z) / l : s + z;
     }
     __syncthreads();
   }
@@ -1062,10 +1166,20 @@ int fast_grid(K kernel, int threads, size_t smem, int64_t work_warps, int wpc) {
   return int(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
+// grids (CTAs resident at once, never more than the work needs)
+template <bool SM>
 int v_grid(const pkv_layer_t* L, int nblocks, int G) {
   const int64_t total = int64_t(L->batch) * L->heads * nblocks;
-  return G <= 4 ? fast_grid(fused_v_fast_kernel<1>, kWV * 32, v_smem_bytes(), total, kWV)
-                : fast_grid(fused_v_fast_kernel<2>, kWV * 32, v_smem_bytes(), total, kWV);
+  return G <= 4 ? fast_grid(fused_v_fast_kernel<1, SM>, kWV * 32, v_smem_bytes(), total, kWV)
+                : fast_grid(fused_v_fast_kernel<2, SM>, kWV * 32, v_smem_bytes(), total, kWV);
+}
+template <bool ST>
+int k_grid(const pkv_layer_t* L, int nblocks, int G) {
+  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
+  const int64_t U = int64_t(L->batch) * L->heads;
+  const int64_t ww = total > U ? total : U;  // at least one warp per unit for the residue
+  return G <= 4 ? fast_grid(fused_k_fast_kernel<1, ST>, kWK * 32, k_smem_bytes(), ww, kWK)
+                : fast_grid(fused_k_fast_kernel<2, ST>, kWK * 32, k_smem_bytes(), ww, kWK);
 }
 // slots per unit: the most warps whose ranges can meet one unit
 int v_maxseg(const pkv_layer_t* L, int nblocks, int64_t nwarps) {
@@ -1074,6 +1188,46 @@ int v_maxseg(const pkv_layer_t* L, int nblocks, int64_t nwarps) {
   const int64_t len_min = total / nwarps;  // every range has len_min or len_min + 1 blocks
   if (len_min == 0) return int(nblocks < nwarps ? nblocks : nwarps) + 1;
   return int((nblocks + len_min - 1) / len_min + 1);
+}
+int64_t v_part_floats(const pkv_layer_t* L, int maxseg, int G, int64_t nwarps) {
+  return int64_t(L->batch) * L->heads * maxseg * G * kPart + nwarps * 8 * kD;
+}
+
+template <bool ST>
+void launch_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride, float* kmax,
+              float* kres, int kslots, cudaStream_t s) {
+  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
+  const int NB = max(1, nblocks);
+  const int grid = k_grid<ST>(L, nblocks, G);
+  if (G <= 4)
+    fused_k_fast_kernel<1, ST><<<grid, kWK * 32, k_smem_bytes(), s>>>(*L, q, G, scores, sstride, NB, total, kmax, kres,
+                                                                       kslots);
+  else
+    fused_k_fast_kernel<2, ST><<<grid, kWK * 32, k_smem_bytes(), s>>>(*L, q, G, scores, sstride, NB, total, kmax, kres,
+                                                                       kslots);
+}
+
+template <bool SM>
+void launch_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out, float* part,
+              const float* kmax, const float* kres, int kslots, int64_t knwarps, cudaStream_t s) {
+  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
+  const int grid = v_grid<SM>(L, nblocks, G);
+  const int64_t nwarps = int64_t(grid) * kWV;
+  const int maxseg = v_maxseg(L, nblocks, nwarps);
+  const int NB = max(1, nblocks);
+  float* vscr = part + int64_t(L->batch) * L->heads * maxseg * G * kPart;
+  if (total > 0) {
+    if (G <= 4)
+      fused_v_fast_kernel<1, SM><<<grid, kWV * 32, v_smem_bytes(), s>>>(*L, w, G, wstride, part, NB, total, maxseg,
+                                                                         vscr, kmax, kres, kslots, knwarps, total);
+    else
+      fused_v_fast_kernel<2, SM><<<grid, kWV * 32, v_smem_bytes(), s>>>(*L, w, G, wstride, part, NB, total, maxseg,
+                                                                         vscr, kmax, kres, kslots, knwarps, total);
+  }
+  const int ug = L->batch * L->heads * G;
+  fused_v_fast_finalize<SM><<<ug < 148 * 4 ? ug : 148 * 4, 512, 0, s>>>(*L, part, w, G, wstride, NB, total, nwarps,
+                                                                          maxseg, out, kmax, kres, kslots, knwarps,
+                                                                          total);
 }
 
 }  // namespace
@@ -1084,44 +1238,42 @@ bool pkv_fast_supported(const pkv_layer_t* L, int G, int64_t stride) {
 
 int pkv_fast_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
                      cudaStream_t s) {
-  const size_t smem = k_smem_bytes();
-  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
-  const int U = L->batch * L->heads;
-  const int NB = max(1, nblocks);
-  const int64_t ww = total > U ? total : U;  // at least one warp per unit for the residue
-  if (G <= 4) {
-    const int grid = fast_grid(fused_k_fast_kernel<1>, kWK * 32, smem, ww, kWK);
-    fused_k_fast_kernel<1><<<grid, kWK * 32, smem, s>>>(*L, q, G, scores, sstride, NB, total);
-  } else {
-    const int grid = fast_grid(fused_k_fast_kernel<2>, kWK * 32, smem, ww, kWK);
-    fused_k_fast_kernel<2><<<grid, kWK * 32, smem, s>>>(*L, q, G, scores, sstride, NB, total);
-  }
+  launch_k<false>(L, nblocks, q, G, scores, sstride, nullptr, nullptr, 0, s);
   return pkv_cuda_status(cudaGetLastError(), "pkv_fused_k_scores(fast)");
 }
 
 int64_t pkv_fast_v_scratch(const pkv_layer_t* L, int nblocks, int G) {
-  const int64_t nwarps = int64_t(v_grid(L, nblocks, G)) * kWV;
-  const int maxseg = v_maxseg(L, nblocks, nwarps);
-  return (int64_t(L->batch) * L->heads * maxseg * G * kPart + nwarps * 8 * kD) * 4;
+  const int64_t nwarps = int64_t(v_grid<false>(L, nblocks, G)) * kWV;
+  return v_part_floats(L, v_maxseg(L, nblocks, nwarps), G, nwarps) * 4;
 }
 
 int pkv_fast_fused_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t wstride, float* out,
                      float* part, cudaStream_t s) {
-  const int64_t total = int64_t(L->batch) * L->heads * nblocks;
-  const int grid = v_grid(L, nblocks, G);
-  const int64_t nwarps = int64_t(grid) * kWV;
-  const int maxseg = v_maxseg(L, nblocks, nwarps);
-  const int NB = max(1, nblocks);
-  float* vscr = part + int64_t(L->batch) * L->heads * maxseg * G * kPart;
-  const size_t smem = v_smem_bytes();
-  if (total > 0) {
-    if (G <= 4)
-      fused_v_fast_kernel<1><<<grid, kWV * 32, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
-    else
-      fused_v_fast_kernel<2><<<grid, kWV * 32, smem, s>>>(*L, w, G, wstride, part, NB, total, maxseg, vscr);
-  }
-  const int ug = L->batch * L->heads * G;
-  fused_v_fast_finalize<<<ug < 148 * 4 ? ug : 148 * 4, 512, 0, s>>>(*L, part, w, G, wstride, NB, total, nwarps, maxseg,
-                                                                      out);
+  launch_v<false>(L, nblocks, w, G, wstride, out, part, nullptr, nullptr, 0, 0, s);
   return pkv_cuda_status(cudaGetLastError(), "pkv_fused_v_output(fast)");
+}
+
+// attention_decode: scores (q pre-scaled by 1/sqrt(d)) with their softmax
+// statistics, then the V pass on exp(s - M) and a normalising finalize.
+// Scratch: kmax [U][kslots][G], kres [U][G], then the V partials.
+int64_t pkv_fast_attention_scratch(const pkv_layer_t* L, int nblocks, int G) {
+  const int64_t U = int64_t(L->batch) * L->heads;
+  const int64_t knw = int64_t(k_grid<true>(L, nblocks, G)) * kWK;
+  const int kslots = v_maxseg(L, nblocks, knw);
+  const int64_t vnw = int64_t(v_grid<true>(L, nblocks, G)) * kWV;
+  const int64_t kf = (U * kslots * G + U * G + 3) / 4 * 4;
+  return (kf + v_part_floats(L, v_maxseg(L, nblocks, vnw), G, vnw)) * 4;
+}
+
+int pkv_fast_attention(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
+                       float* out, float* scratch, cudaStream_t s) {
+  const int64_t U = int64_t(L->batch) * L->heads;
+  const int64_t knw = int64_t(k_grid<true>(L, nblocks, G)) * kWK;
+  const int kslots = v_maxseg(L, nblocks, knw);
+  float* kmax = scratch;
+  float* kres = kmax + U * kslots * G;
+  float* vpart = scratch + (U * kslots * G + U * G + 3) / 4 * 4;
+  launch_k<true>(L, nblocks, q, G, scores, sstride, kmax, kres, kslots, s);
+  launch_v<true>(L, nblocks, scores, G, sstride, out, vpart, kmax, kres, kslots, knw, s);
+  return pkv_cuda_status(cudaGetLastError(), "pkv_attention_decode(fast)");
 }

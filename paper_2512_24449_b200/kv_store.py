@@ -89,6 +89,7 @@ class LayerStore:
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.scratch = torch.empty(0, dtype=torch.uint8, device=dev)
         self.v_scratch = torch.empty(0, dtype=torch.uint8, device=dev)
+        self.a_scratch = torch.empty(0, dtype=torch.uint8, device=dev)
         # host mirrors
         self.nblk_h = 0
         self.nres_h = 0

@@ -369,3 +369,32 @@ def test_graphed_attention_matches_eager_and_recaptures():
         vn = rng.standard_normal((B, 40, H, D)).astype(np.float16)
         st.compress_batch(0, kn, vn)  # 200 -> 240 -> 280: residue and block counts change
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("rels", [(0.1, 0.2), (0.0004, 0.01)])
+@pytest.mark.parametrize("G", [1, 4, 8])
+def test_fused_attention_decode_vs_oracle(rels, G):
+    """pkv_attention_decode (softmax folded into the fused K / V launches) against
+    the f64 oracle softmax(K q / sqrt(d)) V over the dequantized store, with a
+    residue and, at the small rel, wide packs (scalar path, blocks read in place)."""
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    rng = np.random.default_rng(33 + G)
+    B, H, D, T = 2, 2, 128, 64 * 6 + 23
+    k = O.gen_gauss_outlier(rng, B * H * T, D, 4).reshape(B, H, T, D).transpose(0, 2, 1, 3).copy()
+    v = O.gen_gauss_outlier(rng, B * H * T, D, 1).reshape(B, H, T, D).transpose(0, 2, 1, 3).copy()
+    st = CS(1, H, D, batch=B, rel_scale_k=rels[0], rel_scale_v=rels[1])
+    st.compress_batch(0, k, v)
+    q = rng.standard_normal((B, H * G, D)).astype(np.float32) * 3
+    out = attention_decode_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    assert st[0].a_scratch.numel() > 0, "fused attention path not taken"
+    F = __import__("paper_2512_24449_b200.fused_kernels", fromlist=["decode_layer"])
+    Kd = F.decode_layer(st, 0, 0).double().cpu().numpy()  # [B*H, L, D] score order
+    Vd = F.decode_layer(st, 0, 1).double().cpu().numpy()
+    for b in range(B):
+        for hq in range(H * G):
+            u = b * H + hq // G
+            s = Kd[u] @ q[b, hq].astype(np.float64) / np.sqrt(D)
+            p = np.exp(s - s.max())
+            ref = (p / p.sum()) @ Vd[u]
+            _close(out[b, hq], ref)
