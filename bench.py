@@ -195,6 +195,47 @@ def build_store(cfg, rank, repack="none", chunk=4096):
     return st
 
 
+def compressor_bench(cfg, rank, T=4096, appends=128):
+    """The append-time compressor: prefill of T tokens per
+    sequence into a fresh store (quantize + encode + arena append of every
+    block of every (sequence, kv-head), K and V), and single-token decode
+    appends (staging copies; every 64th flushes a block-set).  CUDA-event timed;
+    the fp16 inputs are resident in HBM."""
+    import torch
+    from paper_2512_24449_b200.kv_store import CompressedStore
+    from paper_2512_24449_b200.tensor_model import gauss_outlier
+    B, Hkv, Hq, D, L, _ = cfg
+    k = gauss_outlier((B, T, Hkv, D), n_outlier=4, seed=101 + rank)
+    v = gauss_outlier((B, T, Hkv, D), n_outlier=1, seed=103 + rank)
+    kk = gauss_outlier((B, appends, Hkv, D), n_outlier=4, seed=107 + rank)
+    vv = gauss_outlier((B, appends, Hkv, D), n_outlier=1, seed=109 + rank)
+    res = {}
+    for rep in range(2):  # first pass warms the allocator and the library
+        st = CompressedStore(1, Hkv, D, batch=B, max_tokens=T + appends, check=False)
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        torch.cuda.nvtx.range_push("prefill")
+        st.compress_batch(0, k, v)
+        torch.cuda.nvtx.range_pop()
+        e1.record()
+        for t in range(appends):
+            st.append_token(0, kk[:, t], vv[:, t])
+        e2.record()
+        torch.cuda.synchronize()
+        pre_ms, app_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
+    fp16_in = 2 * B * T * Hkv * D * 2
+    res = {"prefill_tokens": B * T, "prefill_ms": round(pre_ms, 3),
+           "prefill_tokens_per_s": round(B * T / (pre_ms * 1e-3)),
+           "prefill_fp16_in_gbs": round(fp16_in / (pre_ms * 1e-3) / 1e9, 1),
+           "append_us_per_token": round(app_ms * 1e3 / appends, 2),
+           "note": f"batch {B} x {Hkv} kv-heads x {D}, K and V, repack none; appends include "
+                   f"{appends // 64} block-set flushes (host-driven launches)"}
+    del st
+    torch.cuda.empty_cache()
+    return res
+
+
 def cublas_baseline(cfg, rank, reps=10):
     """torch.matmul fp16 (fp32 accumulate) GEMV on the uncompressed cache."""
     import torch
@@ -363,6 +404,7 @@ def main():
     if not args.no_cublas:
         del scores
         cub = cublas_baseline(cfg, rank)
+    comp = compressor_bench(cfg, rank) if not args.no_cublas else None
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(cfg, units=min(8, len(os.sched_getaffinity(0))), L=min(L, 32768), steps=1)
@@ -401,6 +443,8 @@ def main():
                               "v_gbs_equiv": round(logical_kind / (cub["v_us"] * 1e-6) / 1e9, 1),
                               "speedup_k": round(cub["k_us"] / (k_ms * 1e3), 3),
                               "speedup_v": round(cub["v_us"] / (v_ms * 1e3), 3)}
+        if comp:
+            line["compressor"] = comp
         if cb:
             line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)

@@ -468,9 +468,12 @@ struct QFrag {
 template <int NU>
 __device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G, int lane, QFrag<NU>& F) {
   const int gi = lane >> 2, tq = lane & 3;
+  constexpr int GH = 4 * NU;  // heads covered by the fragments (4 or 8)
   float mx[8], sm[8];
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
+  for (int g = 0; g < 8; ++g) mx[g] = sm[g] = 0.f;
+#pragma unroll
+  for (int g = 0; g < GH; ++g) {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (g < G) v = *(const float4*)(qu + g * kD + 4 * lane);
     mx[g] = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
@@ -479,7 +482,7 @@ __device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G,
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
+    for (int g = 0; g < GH; ++g) {
       mx[g] = fmaxf(mx[g], __shfl_xor_sync(PKV_FULL, mx[g], o));
       sm[g] += __shfl_xor_sync(PKV_FULL, sm[g], o);
     }

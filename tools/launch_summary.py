@@ -1,11 +1,14 @@
 """Summarise an ncu --metrics gpu__time_duration.sum launch list (csv)."""
 import csv, sys, collections
-rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 14 and r[0].isdigit()]
+allrows = [r for r in csv.reader(open(sys.argv[1])) if r]
+hdr = next(r for r in allrows if r[0] == "ID")
+ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+rows = [r for r in allrows if r[0].isdigit()]
 agg = collections.OrderedDict()
 for r in rows:
-    name = r[4]
+    name = r[ik]
     short = name.split('(')[0].replace('void ', '').replace('<unnamed>::', '')[:60]
-    v = float(r[14])
+    v = float(r[iv].replace(",", ""))
     a = agg.setdefault(short, [0, 0.0])
     a[0] += 1; a[1] += v
 tot = sum(a[1] for a in agg.values())
