@@ -125,6 +125,9 @@ int pkv_decode_pack_at(const uint8_t* buf, const int64_t* offsets, int32_t n, in
 /* --- store: append_token / compress_batch ------------- */
 /* Scratch bytes needed by pkv_compress_tokens for `nsets` block-sets.      */
 int64_t pkv_compress_scratch_bytes(const pkv_layer_t* L, int32_t nsets);
+/* Same for one repack strategy (PKV_REPACK_*): the default format without
+ * repacking needs ~0.5 KB per block instead of the 16 KB of u16 codes.     */
+int64_t pkv_compress_scratch_bytes_ex(const pkv_layer_t* L, int32_t nsets, int32_t repack);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:
  * [B][ntok][H][D] fp16.  `staged` = tokens already staged per sequence
  * (host mirror of nres, < block); `nblocks_before` = blocks per sequence

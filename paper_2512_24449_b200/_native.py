@@ -54,6 +54,7 @@ _SIGS = {
                              c_void_p]),
     "pkv_decode_pack_at": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
     "pkv_compress_scratch_bytes": (c_int64, [POINTER(Layer), c_int32]),
+    "pkv_compress_scratch_bytes_ex": (c_int64, [POINTER(Layer), c_int32, c_int32]),
     "pkv_compress_tokens": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_int32, c_int32, c_int32, c_float, c_float,
                                       c_int32, c_void_p, c_int64, c_void_p]),
     "pkv_fused_k_scores": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_void_p, c_int64, c_void_p]),
@@ -95,8 +96,16 @@ def load(require_cuda: bool = False):
     return _lib
 
 
+_cuda_ok = False
+
+
 def lib():
-    return load(require_cuda=True)
+    global _cuda_ok
+    if _cuda_ok:
+        return _lib
+    out = load(require_cuda=True)
+    _cuda_ok = True
+    return out
 
 
 def last_error() -> str:
@@ -143,5 +152,11 @@ def ptr(t) -> int:
 
 
 def stream() -> int:
+    """The current CUDA stream of the current device, as a raw handle.  Uses
+    torch's C accessor (torch.cuda.current_stream() builds a Python Stream
+    object and re-validates the device: ~10 us per call on the append path)."""
     import torch
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(torch._C._cuda_getDevice()))
     return int(torch.cuda.current_stream().cuda_stream)

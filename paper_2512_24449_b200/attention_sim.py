@@ -16,7 +16,7 @@ from .fused_kernels import fused_k_scores_batched, fused_v_output_batched, _as_f
 from .kv_store import CompressedStore, ctypes_ref
 
 
-def attention_decode_batched(store: CompressedStore, layer: int, q) -> torch.Tensor:
+def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride: int = 0) -> torch.Tensor:
     """q [B, Hq, D] -> out [B, Hq, D].
 
     The 1/sqrt(d) scale is applied to the (small) query instead of the
@@ -25,7 +25,9 @@ def attention_decode_batched(store: CompressedStore, layer: int, q) -> torch.Ten
     the K launch records per-slot score maxima, the V launch weights rows with
     exp(s - max) and the finalize divides by the sum), so the scores are
     written once and read once; other formats compose fused K -> softmax ->
-    fused V."""
+    fused V.  score_stride (>= the token count) sizes the
+    internal score rows; GraphedAttention passes room for the whole staging
+    ring so one capture serves every residue length."""
     q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
     ls = store[layer]
     B, H, D = store.batch, store.heads, store.head_dim
@@ -36,8 +38,7 @@ def attention_decode_batched(store: CompressedStore, layer: int, q) -> torch.Ten
     st = ls.struct()
     need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(st), ls.nblk_h, Hq))
     if need > 0:
-        L = ls.tokens
-        stride = max(L, 1)
+        stride = max(ls.tokens, score_stride, 1)
         stride = (stride + 3) // 4 * 4
         scores = torch.empty((B, Hq, stride), dtype=torch.float32, device=store.device)
         out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
@@ -55,9 +56,11 @@ def attention_decode_batched(store: CompressedStore, layer: int, q) -> torch.Ten
 class GraphedAttention:
     """attention_decode_batched for one layer, captured into a CUDA graph and
     replayed: a decode step is then one graph launch (fused K, softmax, fused V
-    + finalize) instead of a dozen host-driven launches.  The graph is
-    re-captured whenever the layer's block / residue counts or its device
-    buffers change (every 64 appended tokens, or when the store grows)."""
+    + finalize) instead of a dozen host-driven launches.  The kernels read
+    the residue length from the device (pkv_layer_t.nres), so appends that
+    only stage a token replay the same graph; it is re-captured when the
+    block count or the device buffers change (every 64 appended tokens, or
+    when the store grows)."""
 
     def __init__(self, store: CompressedStore, layer: int):
         self.store, self.layer = store, layer
@@ -68,8 +71,12 @@ class GraphedAttention:
 
     def _state(self, q: torch.Tensor):
         ls = self.store[self.layer]
-        return (ls.nblk_h, ls.nres_h, ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(),
-                tuple(q.shape), q.device)
+        return (ls.nblk_h, ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(), tuple(q.shape),
+                q.device)
+
+    def _stride(self) -> int:
+        st = self.store
+        return st[self.layer].nblk_h * st.block + st.buffer
 
     def __call__(self, q: torch.Tensor) -> torch.Tensor:
         q = _as_f32(q, self.store.device)
@@ -79,11 +86,11 @@ class GraphedAttention:
             side = torch.cuda.Stream(device=q.device)
             side.wait_stream(torch.cuda.current_stream(q.device))
             with torch.cuda.stream(side):  # warm-up outside capture (scratch, occupancy queries)
-                attention_decode_batched(self.store, self.layer, self._q)
+                attention_decode_batched(self.store, self.layer, self._q, self._stride())
             torch.cuda.current_stream(q.device).wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._out = attention_decode_batched(self.store, self.layer, self._q)
+                self._out = attention_decode_batched(self.store, self.layer, self._q, self._stride())
             self._graph, self._key = g, key
         self._q.copy_(q, non_blocking=True)
         self._graph.replay()

@@ -59,8 +59,9 @@ __host__ __device__ inline size_t enc_smem_bytes(const Fmt& f) {
   return size_smem_bytes(f) + round16s(max_block_bytes(f)) + 16;
 }
 
-// In-place exclusive scan of arr[0..n) by the whole CTA (blockDim.x == 256).
-// Returns the total on every thread.  `scratch` holds >= 9 ints.
+// In-place exclusive scan of arr[0..n) by the whole CTA (blockDim.x a multiple
+// of 32, <= 1024).  Returns the total on every thread.  `scratch` holds
+// >= blockDim.x / 32 + 1 ints.
 __device__ inline int32_t cta_exclusive_scan(int32_t* arr, int n, int32_t* scratch) {
   const int t = threadIdx.x, nt = blockDim.x;
   const int chunk = (n + nt - 1) / nt;
@@ -84,7 +85,7 @@ __device__ inline int32_t cta_exclusive_scan(int32_t* arr, int n, int32_t* scrat
       scratch[w] = acc;
       acc += v;
     }
-    scratch[8] = acc;
+    scratch[nt / 32] = acc;
   }
   __syncthreads();
   int32_t run = scratch[wid] + inc - s;
@@ -93,7 +94,7 @@ __device__ inline int32_t cta_exclusive_scan(int32_t* arr, int n, int32_t* scrat
     arr[i] = run;
     run += v;
   }
-  const int32_t total = scratch[8];
+  const int32_t total = scratch[nt / 32];
   __syncthreads();
   return total;
 }

@@ -78,7 +78,8 @@ class LayerStore:
         self.max_blocks = max(1, init_blocks)
         self.blk_max = _round16(max_block_bytes(o.block, o.head_dim, o.pack_size))
         cap = self._expected_bytes(self.max_blocks)
-        self.arena = torch.zeros(cap + 16, dtype=torch.uint8, device=dev)
+        # never read beyond the tail (blocks carry their own zero padding): no fill
+        self.arena = torch.empty(cap + 16, dtype=torch.uint8, device=dev)
         self.tail = torch.zeros(1, dtype=torch.int64, device=dev)
         self.blk_off = torch.full((2, U, self.max_blocks), -1, dtype=torch.int64, device=dev)
         self.blk_len = torch.zeros((2, U, self.max_blocks), dtype=torch.int32, device=dev)
@@ -147,7 +148,7 @@ class LayerStore:
             self.tail_ub = int(self.tail.item())         # synchronise only when it may not fit
             if self.tail_ub + need > self.capacity:
                 newcap = max(2 * self.capacity, self.tail_ub + need + self._expected_bytes(nsets))
-                arena = torch.zeros(newcap + 16, dtype=torch.uint8, device=o.device)
+                arena = torch.empty(newcap + 16, dtype=torch.uint8, device=o.device)
                 arena[:self.tail_ub] = self.arena[:self.tail_ub]
                 self.arena = arena
                 self._struct = None
@@ -171,7 +172,7 @@ class LayerStore:
             self._ensure(nsets)
         L = self.struct()
         if nsets:
-            per_set = int(lib.pkv_compress_scratch_bytes(ctypes_ref(L), 1))
+            per_set = int(lib.pkv_compress_scratch_bytes_ex(ctypes_ref(L), 1, N.REPACK[o.repack]))
             chunk = max(1, min(nsets, (256 << 20) // per_set))
             need = per_set * chunk
             if self.scratch.numel() < need:

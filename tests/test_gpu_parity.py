@@ -166,6 +166,44 @@ def test_store_incremental_equals_batch_and_thresholds():
     assert c[0].tokens == 0
 
 
+@pytest.mark.parametrize("repack", ["none", "v_median", "greedy"])
+def test_store_default_format_fast_path(repack):
+    """64 x 128, k = 16 runs the warp-per-block compressor (store_fast_*):
+    batch > 1, staged residues across calls, repack permutations applied
+    while re-quantizing from the f16 source, bit-exact against the oracle."""
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(11)
+    B, H, D, T = 2, 3, 128, 64 * 5 + 17
+    kk, vv = _kv(rng, T, H, D, batch=B)
+    kk = (kk * rng.uniform(0.01, 30, (B, T, 1, 1))).astype(np.float16)
+    st = CS(1, H, D, batch=B, repack=repack, rel_scale_k=0.03, rel_scale_v=0.07)
+    for a, b in ((0, 30), (30, 31), (31, 200), (200, T)):
+        st.compress_batch(0, kk[:, a:b], vv[:, a:b])
+    for b in range(B):
+        ref = O.OracleStore(1, H, D, repack=repack, rel_k=0.03, rel_v=0.07)
+        ref.compress_batch(0, kk[b], vv[b])
+        assert st[0].stream_bytes(b) == ref.layer_stream(0)
+        got = [(e.kind, e.head, e.byte_len, e.permutation.tolist()) for e in st[0].directory() if e.seq == b]
+        exp = [(e.kind, e.head, e.byte_len, e.permutation.tolist()) for e in ref.directory]
+        assert got == exp
+
+
+def test_store_default_format_errors():
+    pk, _, _, _, CS = _pk()
+    bad = np.zeros((70, 2, 128), np.float16)
+    bad[65, 1, 7] = np.inf
+    st = CS(1, 2, 128)
+    with pytest.raises(pk.errors.NonFiniteValueError):
+        st.compress_batch(0, bad, np.zeros_like(bad))
+    # scale = rel * (max - min) above the f16 range -> WidthOverflowError
+    big = np.zeros((64, 2, 128), np.float16)
+    big[:, :, 0] = -60000
+    big[:, :, 1] = 60000
+    st = CS(1, 2, 128, rel_scale_k=1.0)
+    with pytest.raises(pk.errors.WidthOverflowError):
+        st.compress_batch(0, big, np.zeros_like(big))
+
+
 def test_store_errors():
     pk, _, _, _, CS = _pk()
     st = CS(1, 2, 64)
@@ -368,6 +406,18 @@ def test_graphed_attention_matches_eager_and_recaptures():
         kn = rng.standard_normal((B, 40, H, D)).astype(np.float16)
         vn = rng.standard_normal((B, 40, H, D)).astype(np.float16)
         st.compress_batch(0, kn, vn)  # 200 -> 240 -> 280: residue and block counts change
+    # single-token appends that only stage (280 -> 283, 4 blocks + 24..27
+    # staged): the same graph replays, the kernels read the residue length
+    # from the device
+    q = torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32)).cuda()
+    ga(q)
+    g0 = ga._graph
+    for t in range(3):
+        st.append_token(0, rng.standard_normal((B, H, D)).astype(np.float16),
+                        rng.standard_normal((B, H, D)).astype(np.float16))
+        a = ga(q).clone()
+        assert ga._graph is g0
+        assert torch.equal(a, attention_decode_batched(st, 0, q))
     torch.cuda.synchronize()
 
 
