@@ -128,6 +128,13 @@ int64_t pkv_compress_scratch_bytes(const pkv_layer_t* L, int32_t nsets);
 /* Same for one repack strategy (PKV_REPACK_*): the default format without
  * repacking needs ~0.5 KB per block instead of the 16 KB of u16 codes.     */
 int64_t pkv_compress_scratch_bytes_ex(const pkv_layer_t* L, int32_t nsets, int32_t repack);
+/* append_token when it does not complete a block: stages
+ * one token per sequence (k_new/v_new [B][H][D] fp16) at the device-side
+ * residue count nres[b] and increments it.  Reads no host-side position, so
+ * it can be captured in a CUDA graph and replayed step after step; the
+ * caller runs pkv_compress_tokens for the token that completes a block.
+ * nres[b] >= buffer raises PKV_FLAG_CAPACITY.                              */
+int pkv_stage_token(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new, void* stream);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:
  * [B][ntok][H][D] fp16.  `staged` = tokens already staged per sequence
  * (host mirror of nres, < block); `nblocks_before` = blocks per sequence

@@ -55,6 +55,7 @@ _SIGS = {
     "pkv_decode_pack_at": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
     "pkv_compress_scratch_bytes": (c_int64, [POINTER(Layer), c_int32]),
     "pkv_compress_scratch_bytes_ex": (c_int64, [POINTER(Layer), c_int32, c_int32]),
+    "pkv_stage_token": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_void_p]),
     "pkv_compress_tokens": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_int32, c_int32, c_int32, c_float, c_float,
                                       c_int32, c_void_p, c_int64, c_void_p]),
     "pkv_fused_k_scores": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_void_p, c_int64, c_void_p]),

@@ -16,7 +16,8 @@ from .fused_kernels import fused_k_scores_batched, fused_v_output_batched, _as_f
 from .kv_store import CompressedStore, ctypes_ref
 
 
-def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride: int = 0) -> torch.Tensor:
+def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride: int = 0, scores=None,
+                             out=None) -> torch.Tensor:
     """q [B, Hq, D] -> out [B, Hq, D].
 
     The 1/sqrt(d) scale is applied to the (small) query instead of the
@@ -27,7 +28,8 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     written once and read once; other formats compose fused K -> softmax ->
     fused V.  score_stride (>= the token count) sizes the
     internal score rows; GraphedAttention passes room for the whole staging
-    ring so one capture serves every residue length."""
+    ring so one capture serves every residue length.  scores / out may be
+    preallocated (graph capture without allocations)."""
     q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
     ls = store[layer]
     B, H, D = store.batch, store.heads, store.head_dim
@@ -40,8 +42,11 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     if need > 0:
         stride = max(ls.tokens, score_stride, 1)
         stride = (stride + 3) // 4 * 4
-        scores = torch.empty((B, Hq, stride), dtype=torch.float32, device=store.device)
-        out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
+        if scores is None or scores.shape[-1] < stride:
+            scores = torch.empty((B, Hq, stride), dtype=torch.float32, device=store.device)
+        stride = int(scores.shape[-1])
+        if out is None:
+            out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
         if ls.a_scratch.numel() < need:
             ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=store.device)
         N.check(lib.pkv_attention_decode(ctypes_ref(st), ls.nblk_h, N.ptr(q), Hq, N.ptr(scores), stride, N.ptr(out),
@@ -53,7 +58,47 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     return fused_v_output_batched(store, layer, a)
 
 
-class GraphedAttention:
+class _Captured:
+    """Shared machinery: static input/output buffers allocated OUTSIDE the
+    capture (so capturing allocates nothing), a capture key over the state the
+    recorded launches bake in (block count, device buffers, shapes)."""
+
+    def __init__(self, store: CompressedStore, layer: int):
+        self.store, self.layer = store, layer
+        self._key = None
+        self._graph = None
+        self._scores = None
+        self._out = None
+        self.captures = 0
+
+    def _state(self, q: torch.Tensor):
+        ls = self.store[self.layer]
+        return (ls.nblk_h, ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(), tuple(q.shape),
+                q.device)
+
+    def _buffers(self, q: torch.Tensor):
+        st = self.store
+        # room for every residue length of the current block count
+        stride = (st[self.layer].nblk_h * st.block + st.buffer + 3) // 4 * 4
+        B, Hq, D = q.shape
+        if self._scores is None or self._scores.shape != (B, Hq, stride):
+            self._scores = torch.empty((B, Hq, stride), dtype=torch.float32, device=q.device)
+        if self._out is None or self._out.shape != (B, Hq, D):
+            self._out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
+
+    def _attend(self, q: torch.Tensor) -> torch.Tensor:
+        return attention_decode_batched(self.store, self.layer, q, scores=self._scores, out=self._out)
+
+    def _capture(self, record):
+        """record() enqueues the step's launches; warmed up eagerly by the caller."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            record()
+        self._graph = g
+        self.captures += 1
+
+
+class GraphedAttention(_Captured):
     """attention_decode_batched for one layer, captured into a CUDA graph and
     replayed: a decode step is then one graph launch (fused K, softmax, fused V
     + finalize) instead of a dozen host-driven launches.  The kernels read
@@ -62,38 +107,59 @@ class GraphedAttention:
     block count or the device buffers change (every 64 appended tokens, or
     when the store grows)."""
 
-    def __init__(self, store: CompressedStore, layer: int):
-        self.store, self.layer = store, layer
-        self._key = None
-        self._graph = None
-        self._q = None
-        self._out = None
-
-    def _state(self, q: torch.Tensor):
-        ls = self.store[self.layer]
-        return (ls.nblk_h, ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(), tuple(q.shape),
-                q.device)
-
-    def _stride(self) -> int:
-        st = self.store
-        return st[self.layer].nblk_h * st.block + st.buffer
-
     def __call__(self, q: torch.Tensor) -> torch.Tensor:
         q = _as_f32(q, self.store.device)
         key = self._state(q)
         if key != self._key:
             self._q = q.clone()
-            side = torch.cuda.Stream(device=q.device)
-            side.wait_stream(torch.cuda.current_stream(q.device))
-            with torch.cuda.stream(side):  # warm-up outside capture (scratch, occupancy queries)
-                attention_decode_batched(self.store, self.layer, self._q, self._stride())
-            torch.cuda.current_stream(q.device).wait_stream(side)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._out = attention_decode_batched(self.store, self.layer, self._q, self._stride())
-            self._graph, self._key = g, key
+            self._buffers(q)
+            self._attend(self._q)  # warm-up outside capture (scratch, occupancy queries)
+            self._capture(lambda: self._attend(self._q))
+            self._key = key
         self._q.copy_(q, non_blocking=True)
         self._graph.replay()
+        return self._out
+
+
+class GraphedDecodeStep(_Captured):
+    """One serving decode step for one layer -- append this step's K/V token
+     then attend with q over everything including it
+     -- as ONE CUDA-graph replay: the staging copy
+    (pkv_stage_token, positioned by the device residue count) and the fused
+    attention launches.  The token that completes a 64-token block runs
+    eagerly (compressor: quantize + encode + arena append, then attention)
+    and the next step re-captures (the block count changed)."""
+
+    def __call__(self, k_tok, v_tok, q: torch.Tensor) -> torch.Tensor:
+        st, ls = self.store, self.store[self.layer]
+        q = _as_f32(q, st.device)
+        if ls.nres_h + 1 >= st.block:  # block completes: eager compress + attention
+            st.append_token(self.layer, k_tok, v_tok)
+            self._buffers(q)
+            return self._attend(q)
+        k = st._norm(k_tok, False)
+        v = st._norm(v_tok, False)
+        if st.check:  # SPEC.md:26: non-finite input raises at append time
+            for x in (k, v):
+                N.check(N.lib().pkv_check_finite(N.ptr(x), x.numel(), N.ptr(ls.err), N.stream()), "append")
+            N.raise_flags(int(ls.err.item()), "append")
+        key = self._state(q)
+        if key != self._key:
+            self._k, self._v, self._q = k.clone(), v.clone(), q.clone()
+            self._buffers(q)
+            self._attend(self._q)  # warm-up outside capture (scratch, occupancy queries); appends nothing
+
+            def record():
+                N.check(N.lib().pkv_stage_token(ctypes_ref(ls.struct()), N.ptr(self._k), N.ptr(self._v),
+                                                N.stream()), "stage_token")
+                self._attend(self._q)
+            self._capture(record)
+            self._key = key
+        self._k.copy_(k, non_blocking=True)
+        self._v.copy_(v, non_blocking=True)
+        self._q.copy_(q, non_blocking=True)
+        self._graph.replay()
+        ls.nres_h += 1
         return self._out
 
 

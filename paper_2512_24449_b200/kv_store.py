@@ -168,6 +168,9 @@ class LayerStore:
         nsets = total // o.block
         if total - nsets * o.block > o.buffer:
             raise N.CapacityError("staging overflow")
+        if T == 1 and nsets == 0:
+            self.stage_token(k_new, v_new, check)
+            return
         if nsets:
             self._ensure(nsets)
         L = self.struct()
@@ -185,6 +188,19 @@ class LayerStore:
         self.tail_ub += nsets * 2 * o.batch * o.heads * self.blk_max
         if check:
             N.raise_flags(int(self.err.item()), "compress")
+
+    def stage_token(self, k_new: torch.Tensor, v_new: torch.Tensor, check: bool = False):
+        """One token per sequence that does not complete a block: staged at the
+        device residue count (pkv_stage_token), so the launch is identical
+        every step and can live inside a CUDA graph (GraphedDecodeStep)."""
+        o = self.owner
+        if self.nres_h + 1 >= o.block:
+            raise ValueError("this token completes a block: use compress()")
+        N.check(N.lib().pkv_stage_token(ctypes_ref(self.struct()), N.ptr(k_new), N.ptr(v_new), N.stream()),
+                "stage_token")
+        self.nres_h += 1
+        if check:
+            N.raise_flags(int(self.err.item()), "stage_token")
 
     # -- introspection (synchronising; parity / debug) ----------------------------
     def tables(self):

@@ -448,3 +448,31 @@ def test_fused_attention_decode_vs_oracle(rels, G):
             p = np.exp(s - s.max())
             ref = (p / p.sum()) @ Vd[u]
             _close(out[b, hq], ref)
+
+
+def test_graphed_decode_step_matches_eager():
+    """attention_sim.GraphedDecodeStep (stage token + attention in one graph,
+    eager compressor on block completion) against append_token +
+    attention_decode_batched on a twin store: identical outputs every step and
+    identical streams, across two block completions."""
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeStep, attention_decode_batched
+    rng = np.random.default_rng(23)
+    B, H, D, G = 2, 2, 128, 4
+    k0, v0 = _kv(rng, 100, H, D, batch=B)
+    a, b = CS(1, H, D, batch=B), CS(1, H, D, batch=B)
+    a.compress_batch(0, k0, v0)
+    b.compress_batch(0, k0, v0)
+    step = GraphedDecodeStep(a, 0)
+    for t in range(100):
+        kt = torch.from_numpy(rng.standard_normal((B, H, D)).astype(np.float16)).cuda()
+        vt = torch.from_numpy(rng.standard_normal((B, H, D)).astype(np.float16)).cuda()
+        q = torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32)).cuda()
+        got = step(kt, vt, q).clone()
+        b.append_token(0, kt, vt)
+        assert torch.equal(got, attention_decode_batched(b, 0, q)), f"step {t}"
+    assert a[0].nblk_h == b[0].nblk_h == 3 and a[0].nres_h == b[0].nres_h == 8
+    assert int(a[0].nres[0].item()) == 8
+    for s in range(B):
+        assert a[0].stream_bytes(s) == b[0].stream_bytes(s)
+    assert torch.equal(a[0].stage[:, :, :8], b[0].stage[:, :, :8])
