@@ -57,6 +57,10 @@ enum {
 #define PKV_REPACK_NONE 0
 #define PKV_REPACK_GREEDY 1
 #define PKV_REPACK_V_MEDIAN 2
+/* pkv_compress_tokens only: the permutation rows perm[b][nblocks_before + j]
+ * of the completed block-sets are already filled in by the caller (a plan
+ * computed over the heads of every shard, see pkv_repack_plan).            */
+#define PKV_REPACK_EXTERNAL 3
 
 /*
  * One layer of a batched compressed store (SPEC.md:357-362 CompressedStore,
@@ -135,6 +139,19 @@ int64_t pkv_compress_scratch_bytes_ex(const pkv_layer_t* L, int32_t nsets, int32
  * caller runs pkv_compress_tokens for the token that completes a block.
  * nres[b] >= buffer raises PKV_FLAG_CAPACITY.                              */
 int pkv_stage_token(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new, void* stream);
+/* Repacking across (kv-head) shards: the plan of a block-set is
+ * shared by all heads of a sequence, so a rank holding some
+ * heads quantizes its pending block-sets (pkv_compress_codes: codes
+ * [nsets][B][2][H][block][head_dim] u16, params [...][block][2] f32 -- the
+ * block-sets completed by staged + ntok tokens), all-gathers the codes of all
+ * heads, computes the same plan as every other rank (pkv_repack_plan: codes
+ * in the same layout with H = all heads -> perm [B][nsets][block]) and
+ * compresses with PKV_REPACK_EXTERNAL.  Bytes are identical to one device
+ * holding every head.                                                      */
+int pkv_compress_codes(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new, int32_t ntok,
+                       int32_t staged, float rel_k, float rel_v, uint16_t* codes, float* params, void* stream);
+int pkv_repack_plan(const uint16_t* codes, int32_t nsets, int32_t batch, int32_t heads, int32_t head_dim,
+                    int32_t block, int32_t pack_size, int32_t repack, uint8_t* perm, void* stream);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:
  * [B][ntok][H][D] fp16.  `staged` = tokens already staged per sequence
  * (host mirror of nres, < block); `nblocks_before` = blocks per sequence

@@ -20,6 +20,7 @@ PKV_OK, PKV_E_SHAPE, PKV_E_NONFINITE, PKV_E_WIDTH, PKV_E_MALFORMED = 0, 1, 2, 3,
 PKV_E_INDEX, PKV_E_ARG, PKV_E_CUDA, PKV_E_CAPACITY = 5, 6, 7, 8
 FLAG_NONFINITE, FLAG_WIDTH, FLAG_MALFORMED, FLAG_CAPACITY = 1, 2, 4, 8
 REPACK = {"none": 0, "greedy": 1, "v_median": 2}
+REPACK_EXTERNAL = 3
 
 
 class CapacityError(E.PackKVError):
@@ -56,6 +57,10 @@ _SIGS = {
     "pkv_compress_scratch_bytes": (c_int64, [POINTER(Layer), c_int32]),
     "pkv_compress_scratch_bytes_ex": (c_int64, [POINTER(Layer), c_int32, c_int32]),
     "pkv_stage_token": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_void_p]),
+    "pkv_compress_codes": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_int32, c_int32, c_float, c_float, c_void_p,
+                                     c_void_p, c_void_p]),
+    "pkv_repack_plan": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
+                                  c_void_p]),
     "pkv_compress_tokens": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_int32, c_int32, c_int32, c_float, c_float,
                                       c_int32, c_void_p, c_int64, c_void_p]),
     "pkv_fused_k_scores": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_void_p, c_int64, c_void_p]),

@@ -154,8 +154,11 @@ class LayerStore:
                 self._struct = None
 
     # -- append -----------------------------------------------------------------
-    def compress(self, k_new: torch.Tensor, v_new: torch.Tensor, check: bool):
-        """k_new/v_new: fp16 [B, T, H, D] on the device, contiguous."""
+    def compress(self, k_new: torch.Tensor, v_new: torch.Tensor, check: bool, perm: Optional[torch.Tensor] = None):
+        """k_new/v_new: fp16 [B, T, H, D] on the device, contiguous.  perm
+        ([B, nsets, block] uint8, optional): the repack plan of the block-sets
+        this call completes, computed by the caller (sharded repacking); the
+        store's own strategy is used otherwise."""
         o = self.owner
         T = int(k_new.shape[1])
         lib = N.lib()
@@ -171,23 +174,47 @@ class LayerStore:
         if T == 1 and nsets == 0:
             self.stage_token(k_new, v_new, check)
             return
+        repack = N.REPACK[o.repack]
+        if perm is not None and nsets:
+            if tuple(perm.shape) != (o.batch, nsets, o.block) or perm.dtype != torch.uint8:
+                raise E.ShapeMismatchError(f"perm must be uint8 [{o.batch}, {nsets}, {o.block}]")
+            repack = N.REPACK_EXTERNAL
         if nsets:
             self._ensure(nsets)
+            if repack == N.REPACK_EXTERNAL:
+                self.perm[:, self.nblk_h:self.nblk_h + nsets].copy_(perm)
         L = self.struct()
         if nsets:
-            per_set = int(lib.pkv_compress_scratch_bytes_ex(ctypes_ref(L), 1, N.REPACK[o.repack]))
+            per_set = int(lib.pkv_compress_scratch_bytes_ex(ctypes_ref(L), 1, repack))
             chunk = max(1, min(nsets, (256 << 20) // per_set))
             need = per_set * chunk
             if self.scratch.numel() < need:
                 self.scratch = torch.empty(need, dtype=torch.uint8, device=o.device)
         N.check(lib.pkv_compress_tokens(ctypes_ref(L), N.ptr(k_new), N.ptr(v_new), T, self.nres_h, self.nblk_h,
-                                        float(o.rel_scale_k), float(o.rel_scale_v), N.REPACK[o.repack],
+                                        float(o.rel_scale_k), float(o.rel_scale_v), repack,
                                         N.ptr(self.scratch), int(self.scratch.numel()), strm), "compress")
         self.nblk_h += nsets
         self.nres_h = total - nsets * o.block
         self.tail_ub += nsets * 2 * o.batch * o.heads * self.blk_max
         if check:
             N.raise_flags(int(self.err.item()), "compress")
+
+    def pending_codes(self, k_new: torch.Tensor, v_new: torch.Tensor):
+        """Quantized codes of the block-sets that appending k_new/v_new
+        ([B, T, H, D] fp16, device) would complete, without appending:
+        the u16 codes [nsets, B, 2, H, block, D] stored in an int16 tensor
+        (pkv_compress_codes), or None."""
+        o = self.owner
+        T = int(k_new.shape[1])
+        nsets = (self.nres_h + T) // o.block
+        if nsets == 0:
+            return None
+        codes = torch.empty((nsets, o.batch, 2, o.heads, o.block, o.head_dim), dtype=torch.int16, device=o.device)
+        params = torch.empty((nsets, o.batch, 2, o.heads, o.block, 2), dtype=torch.float32, device=o.device)
+        N.check(N.lib().pkv_compress_codes(ctypes_ref(self.struct()), N.ptr(k_new), N.ptr(v_new), T, self.nres_h,
+                                           float(o.rel_scale_k), float(o.rel_scale_v), N.ptr(codes), N.ptr(params),
+                                           N.stream()), "pending_codes")
+        return codes
 
     def stage_token(self, k_new: torch.Tensor, v_new: torch.Tensor, check: bool = False):
         """One token per sequence that does not complete a block: staged at the

@@ -114,6 +114,56 @@ class ShardedDecoder:
         return assemble(self.p, self._gather)
 
 
+def _all_gather(t: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """[world, *t.shape] gathered copies of t (NCCL: one all_gather_into_tensor)."""
+    out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out.view(-1, *t.shape[1:]) if t.dim() else out, t, group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), t, group=group)
+    return out
+
+
+def gather_codes(codes: torch.Tensor, p: Partition, all_gather) -> torch.Tensor:
+    """This rank's int16 codes [nsets, B, 2, H_loc, block, D] (kv-head split)
+    -> every head's [nsets, B, 2, world * H_loc, block, D], heads in global
+    order.  Exchanged as bytes (NCCL has no 16-bit integer type)."""
+    nsets, B, two, Hl, blk, D = codes.shape
+    g = all_gather(codes.contiguous().view(torch.uint8)).view(torch.int16)
+    g = g.reshape(p.world, nsets, B, two, Hl, blk, D)
+    return g.permute(1, 2, 3, 0, 4, 5, 6).reshape(nsets, B, two, p.world * Hl, blk, D).contiguous()
+
+
+def compress_sharded(store, p: Partition, layer: int, k_local, v_local, all_gather=None, group=None):
+    """compress_batch / append for this rank's units with repacking that
+    matches a single device holding every head:
+    the plan of a block-set is shared by all heads of a sequence, so under a
+    kv-head split each rank quantizes the block-sets the call completes
+    (pkv_compress_codes), the int codes of all heads are all-gathered (as
+    bytes), every rank computes the same plan from them (pkv_repack_plan) and
+    compresses with it (PKV_REPACK_EXTERNAL).  Batch splits and repack "none"
+    need no exchange.  k_local / v_local: [B_loc, T, H_loc, D] fp16.
+    all_gather(t) -> [world, *t.shape] defaults to torch.distributed."""
+    from . import _native as N
+    ls = store[layer]
+    k = store._norm(k_local, True)
+    v = store._norm(v_local, True)
+    if store.repack == "none" or p.mode == "batch" or p.world == 1:
+        ls.compress(k, v, store.check)
+        return
+    codes = ls.pending_codes(k, v)
+    gather = all_gather or (lambda t: _all_gather(t, p.world, group))
+    if codes is None:  # every rank completes the same number of block-sets (lockstep batch)
+        ls.compress(k, v, store.check)
+        return
+    allc = gather_codes(codes, p, gather)
+    nsets, B, _, Hl, blk, D = codes.shape
+    perm = torch.empty((B, nsets, blk), dtype=torch.uint8, device=allc.device)
+    N.check(N.lib().pkv_repack_plan(N.ptr(allc), nsets, B, p.world * Hl, D, blk, store.pack_size,
+                                    N.REPACK[store.repack], N.ptr(perm), N.stream()), "repack_plan")
+    ls.compress(k, v, store.check, perm=perm)
+
+
 def make_local_store(p: Partition, layers: int, head_dim: int, **kw):
     """CompressedStore holding this rank's units (CUDA)."""
     from .kv_store import CompressedStore

@@ -476,3 +476,37 @@ def test_graphed_decode_step_matches_eager():
     for s in range(B):
         assert a[0].stream_bytes(s) == b[0].stream_bytes(s)
     assert torch.equal(a[0].stage[:, :, :8], b[0].stage[:, :, :8])
+
+
+@pytest.mark.parametrize("repack", ["v_median", "greedy"])
+def test_sharded_repack_plan_matches_single_device(repack):
+    """kv-head split with repacking: two simulated ranks holding
+    heads {0,1} and {2,3} exchange codes, compute the shared plan and produce
+    exactly the blocks (bytes and permutations) of one store holding all 4."""
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200 import sharding as S
+    rng = np.random.default_rng(31)
+    B, H, D, T, W = 2, 4, 128, 64 * 3 + 20, 2
+    kk, vv = _kv(rng, T, H, D, batch=B)
+    full = CS(1, H, D, batch=B, repack=repack)
+    parts = [S.plan_partition(B, H, W, r) for r in range(W)]
+    local = [CS(1, p.local_heads, D, batch=B, repack=repack) for p in parts]
+    for a, b in ((0, 70), (70, 150), (150, T)):
+        full.compress_batch(0, kk[:, a:b], vv[:, a:b])
+        ks = [np.ascontiguousarray(kk[:, a:b, p.h0:p.h1]) for p in parts]
+        vs = [np.ascontiguousarray(vv[:, a:b, p.h0:p.h1]) for p in parts]
+        codes = []
+        for st, k1, v1 in zip(local, ks, vs):
+            c = st[0].pending_codes(st._norm(k1, True), st._norm(v1, True))
+            codes.append(None if c is None else c.view(torch.uint8))
+        for st, p, k1, v1 in zip(local, parts, ks, vs):
+            S.compress_sharded(st, p, 0, k1, v1, all_gather=lambda t: torch.stack(codes))
+    fe = {(e.seq, e.kind, e.head, e.token_start): e for e in full[0].directory()}
+    n = 0
+    for st, p in zip(local, parts):
+        for e in st[0].directory():
+            g = fe[(e.seq, e.kind, e.head + p.h0, e.token_start)]
+            assert st[0].block_bytes(e) == full[0].block_bytes(g)
+            assert np.array_equal(e.permutation, g.permutation)
+            n += 1
+    assert n == len(fe) == 3 * B * 2 * H

@@ -95,3 +95,30 @@ def test_plan_partition_rules():
     p0 = S.plan_partition(3, 4, 2, 0, prefer="head")
     a = S.assemble(p0, g)
     assert a.shape == (3, 8, 5) and torch.equal(a[:, 4:], g[1])
+
+
+def _codes_worker(rank, world, port, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nsets, B, H, blk, D = 2, 3, 4, 64, 16
+        full = torch.arange(nsets * B * 2 * H * blk * D, dtype=torch.int32).reshape(nsets, B, 2, H, blk, D)
+        full = (full * 7919 % 65536 - 32768).to(torch.int16)
+        p = S.plan_partition(B, H, world, rank, prefer="head")
+        mine = full[:, :, :, p.h0:p.h1].contiguous()
+        allc = S.gather_codes(mine, p, lambda t: S._all_gather(t, world))
+        ret[rank] = bool(torch.equal(allc, full))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_repack_codes_exchange():
+    """The code exchange behind kv-head-split repacking (sharding.compress_sharded):
+    every rank reassembles all heads' codes in global head order."""
+    world = 2
+    mgr = mp.get_context("spawn").Manager()
+    ret = mgr.dict()
+    mp.start_processes(_codes_worker, args=(world, _free_port(), ret), nprocs=world, start_method="spawn",
+                       join=True)
+    assert all(ret[r] for r in range(world))
