@@ -26,6 +26,7 @@ Arithmetic conventions:
 from __future__ import annotations
 
 import itertools
+import struct
 import math
 import os
 from dataclasses import dataclass, field
@@ -734,3 +735,126 @@ def generate_synthetic(mode: str, seed: int, layers: int, heads: int, head_dim: 
 
 def threads() -> int:
     return int(os.environ.get("PACKKV_THREADS", len(os.sched_getaffinity(0))))
+
+
+# --------------------------------------------------------------------------
+# file formats (test infrastructure restatements)
+# --------------------------------------------------------------------------
+# KV dump, SPEC.md:40-57 (ops) and :82 (layout): "PKKV" | version u16 = 1 |
+# layers u16 | heads u16 | head_dim u16 | tokens u32 | per (layer, head): K then
+# V, tokens x head_dim raw f16, row-major, little-endian, no padding.
+_DUMP_HDR = struct.Struct("<4sHHHHI")
+
+
+def write_dump(k, v, path):
+    """k, v: [layers, heads, tokens, head_dim] float16 arrays."""
+    k = np.asarray(k, np.float16)
+    v = np.asarray(v, np.float16)
+    L, H, T, D = k.shape
+    with open(path, "wb") as f:
+        f.write(_DUMP_HDR.pack(b"PKKV", 1, L, H, D, T))
+        for l in range(L):
+            for h in range(H):
+                f.write(k[l, h].astype("<f2").tobytes())
+                f.write(v[l, h].astype("<f2").tobytes())
+
+
+def read_dump(path):
+    """SPEC.md:40-48: (k, v) [layers, heads, tokens, head_dim] f16; distinct
+    errors for bad magic, truncation and non-finite values."""
+    data = open(path, "rb").read()
+    if len(data) < 4 or data[:4] != b"PKKV":
+        raise _E.BadMagicError("not a PKKV dump")
+    if len(data) < _DUMP_HDR.size:
+        raise _E.TruncatedDumpError("header truncated")
+    _, ver, L, H, D, T = _DUMP_HDR.unpack_from(data)
+    if ver != 1:
+        raise _E.DumpFormatError(f"unsupported dump version {ver}")
+    n = L * H * T * D
+    if len(data) < _DUMP_HDR.size + 4 * n:
+        raise _E.TruncatedDumpError("payload truncated")
+    if len(data) > _DUMP_HDR.size + 4 * n:
+        raise _E.DumpFormatError("trailing bytes after the payload")
+    a = np.frombuffer(data, "<f2", count=2 * n, offset=_DUMP_HDR.size).reshape(L, H, 2, T, D)
+    if not np.all(np.isfinite(a.astype(np.float32))):
+        raise _E.NonFiniteValueError("non-finite value in dump")
+    return a[:, :, 0].astype(np.float16), a[:, :, 1].astype(np.float16)
+
+
+# Compressed store file "PKKS" v1 (SPEC.md:419: header + arena + directory;
+# the field layout is the builder's, documented in DESIGN.md §3.1).  One
+# sequence here (batch = 1); arena offsets 16-byte aligned, zero padding.
+_PKKS_HDR = struct.Struct("<4sHHHHHHHHB3xff")
+_PKKS_LAYER = struct.Struct("<IIQ")
+_PKKS_REC = struct.Struct("<QI")
+_REPACK_CODE = {"none": 0, "greedy": 1, "v_median": 2}
+
+
+def save_pkks(store: "OracleStore", path):
+    out = bytearray(_PKKS_HDR.pack(b"PKKS", 1, store.layers, 1, store.heads, store.head_dim, store.block,
+                                   store.pack_size, store.buffer, _REPACK_CODE[store.repack],
+                                   np.float32(store.rel_k), np.float32(store.rel_v)))
+    for l in range(store.layers):
+        ents = [e for e in store.directory if e.layer == l]   # order (block-set, kind, head)
+        nblk = len(ents) // (2 * store.heads)
+        nres = store.stage_k[l].shape[0]
+        arena, recs, perms = bytearray(), [], []
+        for i, e in enumerate(ents):
+            recs.append((len(arena), e.byte_len))
+            arena += store.block_bytes(e)
+            arena += bytes(-len(arena) % 16)
+            if i % (2 * store.heads) == 0:
+                perms.append(np.asarray(e.permutation, np.uint8))
+        out += _PKKS_LAYER.pack(nblk, nres, len(arena))
+        out += arena
+        for r in recs:
+            out += _PKKS_REC.pack(*r)
+        for p in perms:
+            out += p.tobytes()
+        for st in (store.stage_k[l], store.stage_v[l]):      # [nres, H, D] -> per head
+            for h in range(store.heads):
+                out += np.ascontiguousarray(st[:, h, :]).astype("<f2").tobytes()
+    open(path, "wb").write(bytes(out))
+
+
+def load_pkks(path) -> "OracleStore":
+    try:
+        return _load_pkks(open(path, "rb").read())
+    except (ValueError, struct.error, KeyError) as e:
+        raise _E.StoreFormatError(f"malformed PKKS file: {e}") from e
+
+
+def _load_pkks(data: bytes) -> "OracleStore":
+    if data[:4] != b"PKKS" or len(data) < _PKKS_HDR.size:
+        raise _E.StoreFormatError("not a PKKS store file")
+    (_, ver, layers, batch, heads, head_dim, block, k, buffer, rep, rel_k,
+     rel_v) = _PKKS_HDR.unpack_from(data)
+    if ver != 1 or batch != 1:
+        raise _E.StoreFormatError("unsupported PKKS version or batch")
+    repack = {v: s for s, v in _REPACK_CODE.items()}[rep]
+    st = OracleStore(layers, heads, head_dim, float(rel_k), float(rel_v), k, repack, block, buffer)
+    pos = _PKKS_HDR.size
+    for l in range(layers):
+        nblk, nres, alen = _PKKS_LAYER.unpack_from(data, pos)
+        pos += _PKKS_LAYER.size
+        arena = data[pos:pos + alen]
+        pos += alen
+        recs = [_PKKS_REC.unpack_from(data, pos + i * _PKKS_REC.size) for i in range(nblk * 2 * heads)]
+        pos += len(recs) * _PKKS_REC.size
+        perms = [np.frombuffer(data, np.uint8, block, pos + j * block).astype(np.int64) for j in range(nblk)]
+        pos += nblk * block
+        for i, (off, ln) in enumerate(recs):
+            j, r = divmod(i, 2 * heads)
+            kind, h = divmod(r, heads)
+            st.directory.append(DirEntry(kind, l, h, j * block, (j + 1) * block, len(st.arena), ln, perms[j]))
+            st.arena += arena[off:off + ln]
+        st.flushed[l] = nblk * block
+        sk = np.frombuffer(data, "<f2", heads * nres * head_dim, pos).reshape(heads, nres, head_dim)
+        pos += sk.nbytes
+        sv = np.frombuffer(data, "<f2", heads * nres * head_dim, pos).reshape(heads, nres, head_dim)
+        pos += sv.nbytes
+        st.stage_k[l] = sk.transpose(1, 0, 2).astype(np.float16)
+        st.stage_v[l] = sv.transpose(1, 0, 2).astype(np.float16)
+    if pos != len(data):
+        raise _E.StoreFormatError("trailing or missing bytes")
+    return st

@@ -390,3 +390,119 @@ def iterate_blocks(store: CompressedStore, layer: int, kind: int, seq: int = 0):
 
 def snapshot_stats(store: CompressedStore, include_staging: bool = False):
     return store.snapshot_stats(include_staging)
+
+
+# ----------------------------------------------------------------------------
+# "PKKS" store file (header + arena bytes + directory records;
+# field layout in DESIGN.md §3.1).  Little-endian:
+#   header  "PKKS" | version u16 = 1 | layers u16 | batch u16 | heads u16 |
+#           head_dim u16 | block u16 | pack_size u16 | buffer u16 | repack u8 |
+#           3 x 0 | rel_k f32 | rel_v f32                             (32 B)
+#   per layer:
+#           nblk u32 (block-sets per sequence) | nres u32 | arena_len u64
+#           arena bytes (blocks at 16-byte aligned offsets, zero padding)
+#           records (offset u64, len u32), arena order (block-set, sequence,
+#             kind, head)
+#           permutations u8 [batch][nblk][block]
+#           staging f16 [batch][kind][head][nres][head_dim]
+# Writing a store and loading it back is a bit-exact round trip; the file of
+# a single-sequence store equals the oracle's (oracle/packkv_oracle.save_pkks).
+# ----------------------------------------------------------------------------
+import struct as _struct
+
+_PKKS_HDR = _struct.Struct("<4sHHHHHHHHB3xff")
+_PKKS_LAYER = _struct.Struct("<IIQ")
+_PKKS_REC = np.dtype([("off", "<u8"), ("len", "<u4")])
+
+
+def save_store(store: CompressedStore, path) -> None:
+    """Serialize every layer (synchronises the device)."""
+    o = store
+    with open(path, "wb") as f:
+        f.write(_PKKS_HDR.pack(b"PKKS", 1, o.layers, o.batch, o.heads, o.head_dim, o.block, o.pack_size, o.buffer,
+                               N.REPACK[o.repack], o.rel_scale_k, o.rel_scale_v))
+        U = o.batch * o.heads
+        for ls in o.layer_stores:
+            nb, nr = ls.nblk_h, ls.nres_h
+            tail = int(ls.tail.item())
+            f.write(_PKKS_LAYER.pack(nb, nr, tail))
+            f.write(ls.arena[:tail].cpu().numpy().tobytes())
+            off, ln, pm = ls.tables()                               # [2, U, nb], [B, nb, block]
+            rec = np.empty((nb, o.batch, 2, o.heads), _PKKS_REC)
+            rec["off"] = off.reshape(2, o.batch, o.heads, nb).transpose(3, 1, 0, 2)
+            rec["len"] = ln.reshape(2, o.batch, o.heads, nb).transpose(3, 1, 0, 2)
+            f.write(rec.tobytes())
+            f.write(np.ascontiguousarray(pm).tobytes())
+            stage = ls.stage[:, :, :nr].reshape(2, o.batch, o.heads, nr, o.head_dim).permute(1, 0, 2, 3, 4)
+            f.write(stage.contiguous().cpu().numpy().astype("<f2").tobytes())
+            assert U == o.batch * o.heads
+
+
+def load_store(path, device=None, check: bool = True) -> CompressedStore:
+    """Inverse of save_store: a device-resident store in the saved state.
+    StoreFormatError on a malformed file."""
+    with open(path, "rb") as f:
+        data = f.read()
+    if len(data) < _PKKS_HDR.size or data[:4] != b"PKKS":
+        raise E.StoreFormatError(f"{path}: not a PKKS store file")
+    (_, ver, layers, batch, heads, head_dim, block, k, buffer, rep, rel_k, rel_v) = _PKKS_HDR.unpack_from(data)
+    if ver != 1:
+        raise E.StoreFormatError(f"{path}: unsupported version {ver}")
+    names = {v: s for s, v in N.REPACK.items()}
+    if rep not in names:
+        raise E.StoreFormatError(f"{path}: bad repack code {rep}")
+    try:
+        st = CompressedStore(layers, heads, head_dim, batch=batch, rel_scale_k=rel_k, rel_scale_v=rel_v,
+                             pack_size=k, repack=names[rep], block=block, buffer=buffer, device=device, check=check)
+    except ValueError as e:
+        raise E.StoreFormatError(f"{path}: {e}") from e
+    hb = header_bytes(block, head_dim, k)
+    pos = _PKKS_HDR.size
+
+    def take(n):
+        nonlocal pos
+        if pos + n > len(data):
+            raise E.StoreFormatError(f"{path}: truncated")
+        b = data[pos:pos + n]
+        pos += n
+        return b
+
+    for ls in st.layer_stores:
+        nb, nr, alen = _PKKS_LAYER.unpack(take(_PKKS_LAYER.size))
+        if nr > buffer or nr >= block:
+            raise E.StoreFormatError(f"{path}: residue {nr} out of range")
+        arena = np.frombuffer(take(alen), np.uint8)
+        rec = np.frombuffer(take(nb * batch * 2 * heads * _PKKS_REC.itemsize), _PKKS_REC)
+        pm = np.frombuffer(take(batch * nb * block), np.uint8).reshape(batch, nb, block)
+        stage = np.frombuffer(take(batch * 2 * heads * nr * head_dim * 2), "<f2")
+        offs, lens = rec["off"].astype(np.int64), rec["len"].astype(np.int64)
+        if ((offs % 16) != 0).any() or (offs + lens > alen).any() or (lens < hb).any():
+            raise E.StoreFormatError(f"{path}: bad directory record")
+        for i in range(len(offs)):                  # header geometry of every block (SPEC.md:330)
+            o0 = int(offs[i])
+            kind = (i // heads) % 2
+            if (arena[o0] != kind or arena[o0 + 2] != k or int(arena[o0 + 4]) | int(arena[o0 + 5]) << 8 != block
+                    or int(arena[o0 + 6]) | int(arena[o0 + 7]) << 8 != head_dim):
+                raise E.StoreFormatError(f"{path}: block {i} header disagrees with the store geometry")
+        if nb > ls.max_blocks:
+            ls._grow_tables(nb)
+        if alen + 16 > ls.arena.numel():
+            ls.arena = torch.empty(alen + 16, dtype=torch.uint8, device=st.device)
+        ls.arena[:alen].copy_(torch.from_numpy(arena.copy()))
+        ls.tail.fill_(alen)
+        o4 = torch.from_numpy(offs.reshape(nb, batch, 2, heads).transpose(2, 1, 3, 0).reshape(2, batch * heads, nb).copy())
+        l4 = torch.from_numpy(lens.reshape(nb, batch, 2, heads).transpose(2, 1, 3, 0).reshape(2, batch * heads, nb)
+                              .astype(np.int32).copy())
+        ls.blk_off[:, :, :nb].copy_(o4)
+        ls.blk_len[:, :, :nb].copy_(l4)
+        ls.perm[:, :nb].copy_(torch.from_numpy(pm.copy()))
+        ls.nblk.fill_(nb)
+        ls.nres.fill_(nr)
+        if nr:
+            sv = torch.from_numpy(stage.astype(np.float16).reshape(batch, 2, heads, nr, head_dim).copy())
+            ls.stage[:, :, :nr].copy_(sv.permute(1, 0, 2, 3, 4).reshape(2, batch * heads, nr, head_dim))
+        ls.nblk_h, ls.nres_h, ls.tail_ub = nb, nr, alen
+        ls._struct = None
+    if pos != len(data):
+        raise E.StoreFormatError(f"{path}: {len(data) - pos} trailing bytes")
+    return st

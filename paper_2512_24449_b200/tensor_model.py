@@ -1,4 +1,9 @@
-"""Synthetic KV inputs generated on the device.
+"""Tensor containers' file format and synthetic KV inputs.
+
+``read_dump`` / ``write_dump`` implement the "PKKV" KV-dump file
+(layout :82): magic | version u16 = 1 | layers u16 | heads u16
+| head_dim u16 | tokens u32 | per (layer, head) K then V, tokens x head_dim raw
+little-endian f16, no padding.  Arrays are [layers, heads, tokens, head_dim].
 
 ``gauss_outlier`` is the bench workload of BASELINE.md §3: N(0,1) fp16 with
 4/128 K outlier channels per (layer, kv-head) at +-8 + N(0, 2) (fixed sign per
@@ -7,7 +12,52 @@ CUDA generator), generated directly in HBM so large configs need no host copy.
 """
 from __future__ import annotations
 
+import struct
+
+import numpy as np
 import torch
+
+from . import errors as E
+
+_DUMP = struct.Struct("<4sHHHHI")
+
+
+def write_dump(k, v, path) -> None:
+    """SPEC.md:49-57: k, v [layers, heads, tokens, head_dim] fp16 (numpy or torch)."""
+    k = np.asarray(k.cpu() if isinstance(k, torch.Tensor) else k, dtype=np.float16)
+    v = np.asarray(v.cpu() if isinstance(v, torch.Tensor) else v, dtype=np.float16)
+    if k.shape != v.shape or k.ndim != 4:
+        raise E.ShapeMismatchError("k and v must both be [layers, heads, tokens, head_dim]")
+    if not (np.isfinite(k.astype(np.float32)).all() and np.isfinite(v.astype(np.float32)).all()):
+        raise E.NonFiniteValueError("non-finite value in dump")
+    L, H, T, D = k.shape
+    body = np.stack([k, v], axis=2).astype("<f2")         # [L, H, 2, T, D]: K then V per (layer, head)
+    with open(path, "wb") as f:
+        f.write(_DUMP.pack(b"PKKV", 1, L, H, D, T))
+        f.write(body.tobytes())
+
+
+def read_dump(path):
+    """SPEC.md:40-48 -> (k, v) fp16 numpy [layers, heads, tokens, head_dim].
+    BadMagicError / TruncatedDumpError / NonFiniteValueError / DumpFormatError."""
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:4] != b"PKKV":
+        raise E.BadMagicError(f"{path}: not a PKKV dump")
+    if len(data) < _DUMP.size:
+        raise E.TruncatedDumpError(f"{path}: header truncated")
+    _, ver, L, H, D, T = _DUMP.unpack_from(data)
+    if ver != 1:
+        raise E.DumpFormatError(f"{path}: unsupported version {ver}")
+    need = _DUMP.size + 2 * 2 * L * H * T * D
+    if len(data) < need:
+        raise E.TruncatedDumpError(f"{path}: payload truncated ({len(data)} < {need} bytes)")
+    if len(data) > need:
+        raise E.DumpFormatError(f"{path}: {len(data) - need} trailing bytes")
+    body = np.frombuffer(data, "<f2", offset=_DUMP.size).reshape(L, H, 2, T, D)
+    if not np.isfinite(body.astype(np.float32)).all():
+        raise E.NonFiniteValueError(f"{path}: non-finite value")
+    return body[:, :, 0].astype(np.float16), body[:, :, 1].astype(np.float16)
 
 
 def gauss_outlier(shape, head_dim_axis: int = -1, n_outlier: int = 4, amp: float = 8.0, sigma: float = 2.0,

@@ -510,3 +510,59 @@ def test_sharded_repack_plan_matches_single_device(repack):
             assert np.array_equal(e.permutation, g.permutation)
             n += 1
     assert n == len(fe) == 3 * B * 2 * H
+
+
+@pytest.mark.parametrize("repack", ["none", "v_median"])
+def test_pkks_store_file_matches_oracle_and_round_trips(repack, tmp_path):
+    """The "PKKS" store file: the GPU store's file is byte-identical
+    to the oracle's for the same tokens; load -> save is bit-exact; a loaded
+    store attends bit-identically; the oracle reads the GPU's file."""
+    pk, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.kv_store import load_store, save_store
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    rng = np.random.default_rng(41)
+    H, D, T = 2, 128, 64 * 3 + 10
+    kk, vv = _kv(rng, T, H, D)
+    ref = O.OracleStore(2, H, D, repack=repack)
+    st = CS(2, H, D, repack=repack)
+    for layer in range(2):
+        ref.compress_batch(layer, kk[:T - 40 * layer], vv[:T - 40 * layer])
+        st.compress_batch(layer, kk[:T - 40 * layer], vv[:T - 40 * layer])
+    save_store(st, tmp_path / "g.pkks")
+    O.save_pkks(ref, tmp_path / "o.pkks")
+    assert (tmp_path / "g.pkks").read_bytes() == (tmp_path / "o.pkks").read_bytes()
+    ld = load_store(tmp_path / "o.pkks")
+    save_store(ld, tmp_path / "g2.pkks")
+    assert (tmp_path / "g2.pkks").read_bytes() == (tmp_path / "g.pkks").read_bytes()
+    q = torch.from_numpy(rng.standard_normal((1, 4 * H, D)).astype(np.float32)).cuda()
+    for layer in range(2):
+        assert torch.equal(attention_decode_batched(ld, layer, q), attention_decode_batched(st, layer, q))
+    back = O.load_pkks(tmp_path / "g.pkks")
+    for layer in range(2):
+        assert back.layer_stream(layer) == ref.layer_stream(layer)
+    # appends continue identically after a load
+    kn, vn = _kv(rng, 70, H, D)
+    ld.compress_batch(0, kn, vn)
+    st.compress_batch(0, kn, vn)
+    assert ld[0].stream_bytes(0) == st[0].stream_bytes(0)
+    data = (tmp_path / "g.pkks").read_bytes()
+    for bad in (b"XKKS" + data[4:], data[:-3], data + b"\0"):
+        (tmp_path / "bad.pkks").write_bytes(bad)
+        with pytest.raises(pk.errors.StoreFormatError):
+            load_store(tmp_path / "bad.pkks")
+
+
+def test_pkks_batched_round_trip(tmp_path):
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.kv_store import load_store, save_store
+    rng = np.random.default_rng(43)
+    B, H, D = 3, 2, 128
+    kk, vv = _kv(rng, 150, H, D, batch=B)
+    st = CS(1, H, D, batch=B, repack="greedy")
+    st.compress_batch(0, kk, vv)
+    save_store(st, tmp_path / "a.pkks")
+    ld = load_store(tmp_path / "a.pkks")
+    save_store(ld, tmp_path / "b.pkks")
+    assert (tmp_path / "a.pkks").read_bytes() == (tmp_path / "b.pkks").read_bytes()
+    for b in range(B):
+        assert ld[0].stream_bytes(b) == st[0].stream_bytes(b)
