@@ -117,11 +117,6 @@ __device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_
   asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
   return d;
 }
-__device__ __forceinline__ uint32_t shf_r_clamp(uint32_t lo, uint32_t hi, uint32_t s) {
-  uint32_t d;
-  asm("shf.r.clamp.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
-  return d;
-}
 
 // Block reads.  Blocks staged in shared memory are addressed with 32-bit
 // shared-window addresses (LDS, no generic-address arithmetic); a block too
@@ -439,7 +434,13 @@ struct Feed {
 // phase of the ldmatrix hit 8 distinct chunks, i.e. no bank conflicts).
 constexpr int kTile = 4 * 128 * 16;  // 8 KB
 constexpr int kWK = 4;               // warps per CTA
-constexpr int kRBK = 10 * 1024, kNSK = 3;
+#ifndef PKV_RBK  // ring bytes / slots per K warp (-D overrides for tools/exp variants)
+#define PKV_RBK (10 * 1024)
+#endif
+#ifndef PKV_NSK
+#define PKV_NSK 3
+#endif
+constexpr int kRBK = PKV_RBK, kNSK = PKV_NSK;
 using FeedK = Feed<kRBK, kNSK>;
 constexpr size_t kWarpSmemK = (kTile + FeedK::bytes() + 127) / 128 * 128;
 
