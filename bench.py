@@ -353,7 +353,21 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    # the timed launches replay CUDA graphs of the fused K and V calls (a decode
+    # step's launches without Python launch overhead, as GraphedAttention runs)
+    gk, gv = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gk):
+        F.fused_k_scores_batched(st, 0, q, out=scores)
+    with torch.cuda.graph(gv):
+        F.fused_v_output_batched(st, 0, w, out=out)
+    for _ in range(args.warmup):
+        gk.replay()
+        gv.replay()
     K = args.steps
+    # working sets below ~L2 size (config A) are flushed between timed steps by
+    # writing 256 MB; ms_per_step is then the sum of the K and V launch times
+    l2_flush = phys_k + phys_v + 2 * B * Hq * L * 4 < 160 * 2 ** 20
+    flush_buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda") if l2_flush else None
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     if world > 1:
         dist.barrier()
@@ -365,10 +379,12 @@ def main():
         e_end = torch.cuda.Event(enable_timing=True)
         e_start.record()
         for i in range(K):
+            if l2_flush:
+                flush_buf.zero_()
             evs[i][0].record()
-            F.fused_k_scores_batched(st, 0, q, out=scores)
+            gk.replay()
             evs[i][1].record()
-            F.fused_v_output_batched(st, 0, w, out=out)
+            gv.replay()
             evs[i][2].record()
             if world > 1:
                 dist.all_gather_into_tensor(gathered, out)
@@ -384,6 +400,8 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, k_ms, v_ms = (float(x) for x in t.tolist())
+    if l2_flush:
+        ms = k_ms + v_ms
     value = world * 2 * logical_kind / (ms * 1e-3) / 1e9
 
     # ---- e2e through the public API: host q (this rank's shard) -> sharded
@@ -437,7 +455,9 @@ def main():
                        "head_dim": D, "tokens": L, "layers": 1, "rel_k": 0.1, "rel_v": 0.2, "pack_size": 16,
                        "block": 64, "repack": "none", "parallelism": f"(batch, kv-head) shards x{world} ({part.mode} split), NCCL all-gather of outputs",
                        "global_batch": B * world,
-                       "l2": "per-step working set (compressed K+V blocks) exceeds the 126 MB L2"},
+                       "l2": ("working set below L2: 256 MB written between timed steps, ms_per_step = K + V "
+                              "launch times" if l2_flush else
+                              "per-step working set (compressed K+V blocks) exceeds the 126 MB L2")},
             "compression_ratio": {"k": round(cr_k, 4), "v": round(cr_v, 4), "k_wire": round(cr_k_wire, 4),
                                   "v_wire": round(cr_v_wire, 4)},
             "kernels": {"fused_k_us": round(k_ms * 1e3, 2), "fused_v_us": round(v_ms * 1e3, 2),
