@@ -722,25 +722,59 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
     F.refill(L, 0, NB, rg, nk, k, F.tail_after(k), lane);
   }
   if (ST && cur_u >= 0) flush_max(cur_u);
-  // uncompressed residue rows of units u = wid, wid + nwarps, ...
+  // uncompressed residue rows (< 64 per sequence): unit u = wid, wid + nwarps,
+  // ... on one warp, lane per token (independent dot products, no shuffle
+  // chains), the unit's q staged in the warp's tile
   for (int64_t uu = wid; uu < U; uu += nwarps) {
     const int u = int(uu);
     const int b = u / L.heads, h = u - b * L.heads;
     const int nr = L.nres[b];
-    const uint16_t* kr = L.stage + (int64_t(0) * U + u) * L.buffer * kD;
-    const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
-    float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride + int64_t(L.nblk[b]) * kRows;
-    float rm = -INFINITY;  // (lane g keeps head g's residue maximum)
-    for (int t = 0; t < nr; ++t) {
-      for (int g = 0; g < G; ++g) {
-        float a = 0.f;
-        for (int c = lane; c < kD; c += 32) a = fmaf(__half2float(__ushort_as_half(kr[t * kD + c])), qu[g * kD + c], a);
-        a = warp_sum(a);
-        if (lane == 0) srow[int64_t(g) * sstride + t] = a;
-        if (lane == g) rm = fmaxf(rm, a);
+    float rm[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) rm[g] = -INFINITY;
+    if (nr > 0) {
+      const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
+      float* qs = reinterpret_cast<float*>(tile);
+      __syncwarp();
+      for (int i = lane; i < G * kD / 4; i += 32) reinterpret_cast<float4*>(qs)[i] = reinterpret_cast<const float4*>(qu)[i];
+      __syncwarp();
+      float* srow = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride + int64_t(L.nblk[b]) * kRows;
+      for (int t = lane; t < nr; t += 32) {
+        const uint4* kr = reinterpret_cast<const uint4*>(L.stage + (int64_t(u) * L.buffer + t) * kD);
+        float acc[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) acc[g] = 0.f;
+#pragma unroll 4
+        for (int c8 = 0; c8 < kD / 8; ++c8) {
+          const uint4 v = kr[c8];
+          const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x0 = h2f(wv[e] & 0xffff), x1 = h2f(wv[e] >> 16);
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              if (g < G) {
+                const float2 qv = *reinterpret_cast<const float2*>(qs + g * kD + 8 * c8 + 2 * e);
+                acc[g] = fmaf(x1, qv.y, fmaf(x0, qv.x, acc[g]));
+              }
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          if (g < G) {
+            srow[int64_t(g) * sstride + t] = acc[g];
+            rm[g] = fmaxf(rm[g], acc[g]);
+          }
       }
     }
-    if (ST && lane < G) kres[int64_t(u) * G + lane] = rm;
+    if (ST) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        if (g < G) {
+          const float m = warp_max(rm[g]);
+          if (lane == 0) kres[int64_t(u) * G + g] = m;
+        }
+    }
   }
 }
 
@@ -1115,26 +1149,42 @@ __global__ void __launch_bounds__(512) fused_v_fast_finalize(pkv_layer_t L, cons
         l += bl[i];
       }
     }
+    // residue rows (< 64): row t goes to thread group t % 4, 8 loads in flight
+    {
+      const int b = u / L.heads;
+      const int nr = L.nres[b];
+      const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
+      const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
+      if (SM) __syncthreads();  // Msh
+      const float M = SM ? Msh : 0.f;
+      for (int t0 = qq; t0 < nr; t0 += 32) {
+        float pw[8], xv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int t = t0 + 4 * i < nr ? t0 + 4 * i : t0;
+          pw[i] = wr[t];
+          xv[i] = __half2float(__ushort_as_half(vr[t * kD + c]));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (t0 + 4 * i < nr) {
+            const float p = SM ? expf(pw[i] - M) : pw[i];
+            s = fmaf(p, xv[i], s);
+            l += p;
+          }
+      }
+    }
     red[qq][c] = s;
     if (c == 0) {
       red[qq][kD] = z;
-      red[qq][kD + 1] = l;
     }
+    // l: every thread of a group holds the same residue sum; the slot sums sit in c == 0
+    if (c == 0) red[qq][kD + 1] = l;
     __syncthreads();
     if (qq == 0) {
       s = ((red[0][c] + red[1][c]) + red[2][c]) + red[3][c];
       z = ((red[0][kD] + red[1][kD]) + red[2][kD]) + red[3][kD];
       l = ((red[0][kD + 1] + red[1][kD + 1]) + red[2][kD + 1]) + red[3][kD + 1];
-      const int b = u / L.heads;
-      const int nr = L.nres[b];
-      const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
-      const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
-      const float M = SM ? Msh : 0.f;
-      for (int t = 0; t < nr; ++t) {
-        const float p = SM ? expf(wr[t] - M) : wr[t];
-        s = fmaf(p, __half2float(__ushort_as_half(vr[t * kD + c])), s);
-        l += p;
-      }
       out[int64_t(ug) * kD + c] = SM ? (s + z) / l : s + z;
     }
     __syncthreads();
