@@ -145,7 +145,8 @@ class GraphedDecodeStep(_Captured):
             N.raise_flags(int(ls.err.item()), "append")
         key = self._state(q)
         if key != self._key:
-            self._k, self._v, self._q = k.clone(), v.clone(), q.clone()
+            if getattr(self, "_k", None) is None or self._k.shape != k.shape or self._q.shape != q.shape:
+                self._k, self._v, self._q = k.clone(), v.clone(), q.clone()
             self._buffers(q)
             self._attend(self._q)  # warm-up outside capture (scratch, occupancy queries); appends nothing
 
@@ -155,12 +156,25 @@ class GraphedDecodeStep(_Captured):
                 self._attend(self._q)
             self._capture(record)
             self._key = key
-        self._k.copy_(k, non_blocking=True)
-        self._v.copy_(v, non_blocking=True)
-        self._q.copy_(q, non_blocking=True)
+        for dst, src in ((self._k, k), (self._v, v), (self._q, q)):
+            if dst.data_ptr() != src.data_ptr():  # callers may write the inputs() in place
+                dst.copy_(src, non_blocking=True)
         self._graph.replay()
         ls.nres_h += 1
         return self._out
+
+    def inputs(self, q_heads: int):
+        """Static device buffers (k [B, 1, H, D] f16, v, q [B, Hq, D] f32) the
+        graph reads: a caller that writes the step's token and query into
+        them and passes them back skips the three input copies."""
+        st = self.store
+        B, H, D = st.batch, st.heads, st.head_dim
+        if getattr(self, "_k", None) is None or self._q.shape != (B, q_heads, D):
+            self._k = torch.zeros((B, 1, H, D), dtype=torch.float16, device=st.device)
+            self._v = torch.zeros_like(self._k)
+            self._q = torch.zeros((B, q_heads, D), dtype=torch.float32, device=st.device)
+            self._key = None
+        return self._k, self._v, self._q
 
 
 def attention_decode(store: CompressedStore, layer: int, head: int, q) -> torch.Tensor:

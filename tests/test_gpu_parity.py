@@ -471,11 +471,23 @@ def test_graphed_decode_step_matches_eager():
         got = step(kt, vt, q).clone()
         b.append_token(0, kt, vt)
         assert torch.equal(got, attention_decode_batched(b, 0, q)), f"step {t}"
-    assert a[0].nblk_h == b[0].nblk_h == 3 and a[0].nres_h == b[0].nres_h == 8
-    assert int(a[0].nres[0].item()) == 8
+    # in-place inputs: write the token / query into the graph's own buffers
+    kb, vb, qb = step.inputs(H * G)
+    for t in range(3):
+        kt = torch.from_numpy(rng.standard_normal((B, H, D)).astype(np.float16)).cuda()
+        vt = torch.from_numpy(rng.standard_normal((B, H, D)).astype(np.float16)).cuda()
+        q = torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32)).cuda()
+        kb.copy_(kt.view_as(kb))
+        vb.copy_(vt.view_as(vb))
+        qb.copy_(q)
+        got = step(kb, vb, qb).clone()
+        b.append_token(0, kt, vt)
+        assert torch.equal(got, attention_decode_batched(b, 0, q)), f"in-place step {t}"
+    assert a[0].nblk_h == b[0].nblk_h == 3 and a[0].nres_h == b[0].nres_h == 11
+    assert int(a[0].nres[0].item()) == 11
     for s in range(B):
         assert a[0].stream_bytes(s) == b[0].stream_bytes(s)
-    assert torch.equal(a[0].stage[:, :, :8], b[0].stage[:, :, :8])
+    assert torch.equal(a[0].stage[:, :, :11], b[0].stage[:, :, :11])
 
 
 @pytest.mark.parametrize("repack", ["v_median", "greedy"])
@@ -566,3 +578,20 @@ def test_pkks_batched_round_trip(tmp_path):
     assert (tmp_path / "a.pkks").read_bytes() == (tmp_path / "b.pkks").read_bytes()
     for b in range(B):
         assert ld[0].stream_bytes(b) == st[0].stream_bytes(b)
+
+
+def test_store_multi_chunk_prefill_equals_incremental():
+    """A prefill larger than one compressor chunk (the scan keeps <= 12224 block
+    sizes in shared memory: 38 block-sets at B=4, H=40) equals the same tokens
+    appended in single-chunk calls (SPEC.md:374-382 batch/incremental identity)."""
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(51)
+    B, H, D, T = 4, 40, 128, 64 * 45 + 7
+    kk, vv = _kv(rng, T, H, D, batch=B)
+    a, b = CS(1, H, D, batch=B), CS(1, H, D, batch=B)
+    a.compress_batch(0, kk, vv)
+    for s0 in range(0, T, 64 * 10 + 3):
+        b.compress_batch(0, kk[:, s0:s0 + 64 * 10 + 3], vv[:, s0:s0 + 64 * 10 + 3])
+    assert a[0].nblk_h == b[0].nblk_h == 45
+    for s in range(B):
+        assert a[0].stream_bytes(s) == b[0].stream_bytes(s)

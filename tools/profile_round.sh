@@ -11,4 +11,11 @@ ncu --set full --clock-control none --import-source on -k regex:fast_kernel -s 4
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
     -k regex:fast_kernel -s 4 -c 2 --csv --log-file gpurun_out/traffic.csv \
     python bench.py --steps 1 --warmup 3 --no-cublas --no-cpu-baseline > /dev/null 2>&1
-echo done
+echo done-fused
+# compressor: prefill launch list + one full capture of the warp-per-block kernels
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --nvtx \
+    --nvtx-include "prefill/" --csv --log-file gpurun_out/comp_launches.csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:store_fast -c 2 -o gpurun_out/prof_comp \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+echo done-comp

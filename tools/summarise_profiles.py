@@ -126,9 +126,51 @@ def full(tag):
     json.dump(js, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
 
 
+def compressor(tag):
+    """profiles/<tag>_compressor.md: prefill launch list (time, DRAM bytes) and
+    the full-set summary of the warp-per-block compressor kernels."""
+    path = os.path.join(OUT, "comp_launches.csv")
+    if not os.path.exists(path):
+        return
+    allrows = [r for r in csv.reader(open(path)) if r]
+    hdr = next(r for r in allrows if r[0] == "ID")
+    ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    per = defaultdict(lambda: defaultdict(list))
+    for r in allrows:
+        if r[0].isdigit():
+            per[short(r[ik])][r[im]].append(float(r[iv].replace(",", "")))
+    lines = [f"# Compressor profile ({tag})", "",
+             "Prefill of 4096 tokens x batch 8 x 8 kv-heads x 128 (K and V, repack none) in bench.py's compressor "
+             "leg; `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --nvtx "
+             "--nvtx-include prefill/` (cold cache, serialised; both prefill repetitions listed)", "",
+             "| kernel | launches | mean us | DRAM read MB | DRAM write MB |", "|---|---|---|---|---|"]
+    for k, m in per.items():
+        t = m.get("gpu__time_duration.sum", [0])
+        rd = m.get("dram__bytes_read.sum", [0])
+        wr = m.get("dram__bytes_write.sum", [0])
+        lines.append(f"| `{k}` | {len(t)} | {sum(t) / len(t) / 1e3:.1f} | {sum(rd) / len(rd) / 1e6:.1f} | "
+                     f"{sum(wr) / len(wr) / 1e6:.1f} |")
+    rep = os.path.join(OUT, "prof_comp.ncu-rep")
+    if os.path.exists(rep):
+        rows = ncu_csv(["-i", rep, "--page", "raw", "--csv"])
+        h = rows[0]
+        want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+                "launch__registers_per_thread", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
+        lines += ["", "## ncu --set full (one launch each)", ""]
+        for r in rows[2:]:
+            lines += [f"### `{short(r[h.index('Kernel Name')])}`", "", "| metric | value |", "|---|---|"]
+            lines += [f"| {m} | {r[h.index(m)]} |" for m in want if m in h]
+            lines.append("")
+    open(os.path.join(PROF, f"{tag}_compressor.md"), "w").write("\n".join(lines) + "\n")
+
+
 if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
     full(tag)
+    compressor(tag)
     print(open(os.path.join(PROF, "ncu_traffic.json")).read())
