@@ -175,6 +175,9 @@ __device__ __forceinline__ void spread8(uint32_t x, const uint4& c, uint32_t mr,
   rb = imad(ub & c.w, 1u, mr);
 }
 
+#ifndef PKV_W2PRED
+#define PKV_W2PRED 0
+#endif
 // Shared-memory operands of one pack: the 3 words covering its <= 64-bit
 // payload (payload starts at bit `bit` of the block, bit % 16 == 0) and the
 // width's table entry.  Issued one pack ahead of the arithmetic.
@@ -188,9 +191,17 @@ __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ l
   PackLd r;
   r.w0 = ld32(p);
   r.w1 = ld32(p + 4);
+#if PKV_W2PRED
   // the payload (16w bits from bit % 32 in {0, 16}) needs a third word only
   // for w = 4 starting mid-word; other lanes skip the load (no bank traffic)
   r.w2 = (w16 == 64u && (bit & 16u)) ? ld32(p + 8) : 0u;
+#else
+  // the payload (16w bits from bit % 32 in {0, 16}) reaches a third word only
+  // for w = 4 starting mid-word; loading it unconditionally (the ring keeps 16
+  // bytes of slack past every block) saves the predicate arithmetic, and the
+  // extra bits fall outside the 16 fields
+  r.w2 = ld32(p + 8);
+#endif
   r.c = *(const uint4*)(lut + w16);  // (computing the constants instead measured slower)
   return r;
 }
@@ -972,7 +983,9 @@ __global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L
       for (int e8 = 0; e8 < TPL / 8; ++e8) {
         uint32_t v[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(__fmaf_rz(xs[8 * e8 + e], f, 8388608.f));
+        // round to nearest (unbiased: a softmax-weighted block sums many small
+        // x·f with errors of both signs), clamped so 65535.5+ cannot carry
+        for (int e = 0; e < 8; ++e) v[e] = min(__float_as_uint(__fmaf_rn(xs[8 * e8 + e], f, 8388608.f)), 0x4B00FFFFu);
         // byte position p holds row tok(p): (0,1,4,5) then (2,3,6,7)
         const uint32_t t01 = __byte_perm(v[0], v[1], 0x5140), t45 = __byte_perm(v[4], v[5], 0x5140);
         const uint32_t t23 = __byte_perm(v[2], v[3], 0x5140), t67 = __byte_perm(v[6], v[7], 0x5140);

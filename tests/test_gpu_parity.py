@@ -361,7 +361,7 @@ def test_attention_decode_singleton():
 
 
 @pytest.mark.parametrize("rels", [(0.1, 0.2), (0.02, 0.05), (0.0004, 0.01)])
-@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 6, 8])
 def test_fused_default_format_paths(rels, G):
     """k=16, D=128 runs the tensor-core kernels; wide packs (w > 5) and codes
     above 2047 exercise their in-launch scalar path."""
@@ -422,7 +422,7 @@ def test_graphed_attention_matches_eager_and_recaptures():
 
 
 @pytest.mark.parametrize("rels", [(0.1, 0.2), (0.0004, 0.01)])
-@pytest.mark.parametrize("G", [1, 4, 8])
+@pytest.mark.parametrize("G", [1, 3, 4, 5, 8])
 def test_fused_attention_decode_vs_oracle(rels, G):
     """pkv_attention_decode (softmax folded into the fused K / V launches) against
     the f64 oracle softmax(K q / sqrt(d)) V over the dequantized store, with a
@@ -595,3 +595,49 @@ def test_store_multi_chunk_prefill_equals_incremental():
     assert a[0].nblk_h == b[0].nblk_h == 45
     for s in range(B):
         assert a[0].stream_bytes(s) == b[0].stream_bytes(s)
+
+
+@pytest.mark.parametrize("T", [1, 5, 63, 64, 65, 128])
+def test_fused_default_format_block_boundaries(T):
+    """Residue-only stores, exact block multiples and one token past them on the
+    default-format kernels (fused K / V and the folded-softmax attention)."""
+    _, _, F, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    rng = np.random.default_rng(60 + T)
+    B, H, D, G = 2, 2, 128, 4
+    st = CS(1, H, D, batch=B)
+    kk, vv = _kv(rng, T, H, D, batch=B)
+    st.compress_batch(0, kk, vv)
+    q = rng.standard_normal((B, H * G, D)).astype(np.float32)
+    w = rng.random((B, H * G, T)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+    a = attention_decode_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    for b in range(B):
+        ref = _oracle_per_seq(kk[b], vv[b], H, D, 16)
+        for hq in range(H * G):
+            rs = O.naive_k_scores(ref, 0, hq // G, q[b, hq])
+            _close(s[b, hq], rs)
+            _close(o[b, hq], O.naive_v_output(ref, 0, hq // G, w[b, hq]))
+            p = np.exp(rs / np.sqrt(D) - (rs / np.sqrt(D)).max())
+            _close(a[b, hq], O.naive_v_output(ref, 0, hq // G, (p / p.sum()).astype(np.float64)))
+
+
+def test_fused_many_heads_config_d_shape():
+    """52 kv-heads (the LLaMA-30B shape of config D), MHA, ragged residue."""
+    _, _, F, _, CS = _pk()
+    rng = np.random.default_rng(71)
+    H, D, T = 52, 128, 64 * 2 + 9
+    kk, vv = _kv(rng, T, H, D)
+    ref = O.OracleStore(1, H, D)
+    ref.compress_batch(0, kk, vv)
+    st = CS(1, H, D)
+    st.compress_batch(0, kk, vv)
+    assert st[0].stream_bytes(0) == ref.layer_stream(0)
+    q = rng.standard_normal((1, H, D)).astype(np.float32)
+    w = rng.random((1, H, T)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+    for h in range(0, H, 7):
+        _close(s[0, h], O.naive_k_scores(ref, 0, h, q[0, h]))
+        _close(o[0, h], O.naive_v_output(ref, 0, h, w[0, h]))
