@@ -158,6 +158,49 @@ def cpu_baseline(cfg, units: int, L: int, steps: int = 1):
                       f"{units} processes", "seconds_per_step": t}
 
 
+def parity_sample(cfg, L: int = 4096):
+    """Part of the cpu_baseline leg: one (sequence, kv-head) unit of the bench
+    distribution compressed by the CPU oracle and by the device, then the
+    device's fused K, fused V and folded-softmax attention against the oracle's
+    f64 naive results.  Reports stream/CR bit-exactness and max abs / norm-rel
+    errors (north star: "max abs/rel error reported")."""
+    import numpy as np
+    import torch
+    from oracle import packkv_oracle as O
+    from paper_2512_24449_b200 import fused_kernels as F
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    from paper_2512_24449_b200.kv_store import CompressedStore
+    B, Hkv, Hq, D, _, _ = cfg
+    G = Hq // Hkv
+    rng = np.random.default_rng(2024)
+    K = O.gen_gauss_outlier(rng, L, D, max(1, D * 4 // 128))[:, None, :]
+    V = O.gen_gauss_outlier(rng, L, D, max(1, D // 128))[:, None, :]
+    ref = O.OracleStore(1, 1, D)
+    ref.compress_batch(0, K, V)
+    st = CompressedStore(1, 1, D)
+    st.compress_batch(0, K, V)
+    q = rng.standard_normal((1, G, D)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()[0]
+    rs = np.stack([O.naive_k_scores(ref, 0, 0, q[0, g]) for g in range(G)])
+    w = np.stack([O.softmax64(rs[g] / math.sqrt(D)) for g in range(G)]).astype(np.float32)
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w[None])).cpu().numpy()[0]
+    ro = np.stack([O.naive_v_output(ref, 0, 0, w[g]) for g in range(G)])
+    a = attention_decode_batched(st, 0, torch.from_numpy(q)).cpu().numpy()[0]
+    ra = np.stack([O.naive_v_output(ref, 0, 0, O.softmax64(rs[g] / math.sqrt(D))) for g in range(G)])
+
+    def err(x, r):
+        e = np.abs(x.astype(np.float64) - r)
+        return {"max_abs": float(e.max()), "max_rel_to_norm": float(e.max() / np.abs(r).max()),
+                "pass": bool(e.max() <= 1e-3 * np.abs(r).max())}
+    phys = sum(e.byte_len for e in ref.directory)
+    return {"sample": f"1 (sequence, kv-head) unit x {L} tokens of the bench distribution, G={G}; "
+                      "oracle = oracle/packkv_oracle.py (f64 naive GEMVs over its own compressed store)",
+            "stream_bit_exact": st[0].stream_bytes(0) == ref.layer_stream(0),
+            "cr_wire_equal": sum(int(x) for x in st[0].tables()[1].ravel()) == phys,
+            "tolerance": "max|gpu - f64| <= 1e-3 * max|f64| (SPEC.md:454,463)",
+            "fused_k": err(s, rs), "fused_v": err(o, ro), "attention": err(a, ra)}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -453,6 +496,7 @@ def main():
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(cfg, units=min(8, len(os.sched_getaffinity(0))), L=min(L, 32768), steps=1)
+        cb["parity"] = parity_sample(cfg)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
