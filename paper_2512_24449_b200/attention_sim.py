@@ -90,10 +90,25 @@ class _Captured:
         return attention_decode_batched(self.store, self.layer, q, scores=self._scores, out=self._out)
 
     def _capture(self, record):
-        """record() enqueues the step's launches; warmed up eagerly by the caller."""
+        """record() enqueues the step's launches; warmed up eagerly by the caller.
+        Captures with CUDAGraph.capture_begin/end on a side stream rather than the
+        torch.cuda.graph context manager, which also runs gc.collect() and
+        empty_cache() (milliseconds) at every re-capture; the launches allocate
+        nothing, and one memory pool is shared by all captures of this object."""
+        dev = torch.device(self.store.device)
+        if getattr(self, "_pool", None) is None:
+            self._pool = torch.cuda.graph_pool_handle()
+            self._side = torch.cuda.Stream(device=dev)
+        cur = torch.cuda.current_stream(dev)
+        self._side.wait_stream(cur)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            record()
+        with torch.cuda.stream(self._side):
+            g.capture_begin(pool=self._pool)
+            try:
+                record()
+            finally:
+                g.capture_end()
+        cur.wait_stream(self._side)
         self._graph = g
         self.captures += 1
 
