@@ -445,6 +445,21 @@ struct Feed {
 // phase of the ldmatrix hit 8 distinct chunks, i.e. no bank conflicts).
 constexpr int kTile = 4 * 128 * 16;  // 8 KB
 constexpr int kWK = 4;               // warps per CTA
+// Diagnostic builds (tools/exp/build_variant.sh -D...; results are wrong, timing
+// only): skip the unpack arithmetic, skip the MMA + epilogue, keep
+// only the feed, or record per-warp feed-wait cycles into the scores buffer.
+#ifndef PKV_DIAG_NODECODE
+#define PKV_DIAG_NODECODE 0
+#endif
+#ifndef PKV_DIAG_NOMMA
+#define PKV_DIAG_NOMMA 0
+#endif
+#ifndef PKV_DIAG_FEEDONLY
+#define PKV_DIAG_FEEDONLY 0
+#endif
+#ifndef PKV_DIAG_WAITCLK
+#define PKV_DIAG_WAITCLK 0
+#endif
 #ifndef PKV_RBK  // ring bytes / slots per K warp (-D overrides for tools/exp variants)
 #define PKV_RBK (10 * 1024)
 #endif
@@ -591,6 +606,10 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   };
   Cursor cs;
   cs.init(rg.b0, NB);
+#if PKV_DIAG_WAITCLK
+  long long dwait = 0;
+  const long long tstart = clock64();
+#endif
   F.refill(L, 0, NB, rg, nk, -1, 0u, lane);
 
 #pragma unroll 1
@@ -605,8 +624,19 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
       build_qfrag<NU>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, Q);
     }
     const uint8_t* gblk;
+#if PKV_DIAG_WAITCLK
+    const long long tw0 = clock64();
+#endif
     const uint32_t blk = F.wait(k, &gblk);
+#if PKV_DIAG_WAITCLK
+    dwait += clock64() - tw0;
+#endif
+#if PKV_DIAG_FEEDONLY
+    if (j < nbk && lane == 0) sbase[j] = __uint_as_float(ld32(blk));
+    if (false) {
+#else
     if (j < nbk) {
+#endif
       Chunk ch;
       const bool fast = gblk == nullptr && parse_chunk(blk, lane, lane, ch);
       if (fast) {
@@ -627,8 +657,13 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
             nB = pack_load(blk, lutb, nbit + nwa, nwb);
           }
           uint32_t ra[4], rb[4];
+#if PKV_DIAG_NODECODE
+          ra[0] = A.w0 ^ bitA; ra[1] = A.w1; ra[2] = A.w2; ra[3] = A.c.x;
+          rb[0] = B.w0 ^ bitB; rb[1] = B.w1; rb[2] = B.w2; rb[3] = B.c.x;
+#else
           pack_decode(A, bitA, min_rep(ch.mn, i2), ra);
           pack_decode(B, bitB, min_rep(ch.mn, i2 + 1), rb);
+#endif
           *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
           *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
           bit = nbit;
@@ -649,6 +684,9 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
         __syncwarp();
         float* p0 = sbase + int64_t(tq) * sstride + j * kRows + tok(gi);  // rows 16g + tok(gi) (+8) of head tq
         float* p1 = p0 + 4 * sstride;                                     // head tq + 4
+#if PKV_DIAG_NOMMA
+        if (tq < G) p0[0] = __uint_as_float(ld32(tile_s + 16u * lane)) + __uint_as_float(prm[0][0]);
+#else
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           int accU[NU][4], accS[4];
@@ -689,6 +727,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
             if (ST) kmx1 = fmaxf(kmx1, fmaxf(scA, scB));
           }
         }
+#endif
         __syncwarp();  // tile reads done before the next block's stores
       } else {
         // scalar path (rare): lane computes rows lane and lane+32 for every head
@@ -733,6 +772,16 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
     F.refill(L, 0, NB, rg, nk, k, F.tail_after(k), lane);
   }
   if (ST && cur_u >= 0) flush_max(cur_u);
+#if PKV_DIAG_WAITCLK
+  __syncwarp();
+  if (lane == 0) {  // (wait cycles, loop cycles, blocks) per warp at the start of scores
+    long long* dbg = reinterpret_cast<long long*>(scores) + 3 * wid;
+    dbg[0] = dwait;
+    dbg[1] = clock64() - tstart;
+    dbg[2] = nk;
+  }
+  return;
+#endif
   // uncompressed residue rows (< 64 per sequence): unit u = wid, wid + nwarps,
   // ... on one warp, lane per token (independent dot products, no shuffle
   // chains), the unit's q staged in the warp's tile
