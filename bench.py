@@ -388,6 +388,14 @@ def main():
     alg_k = phys_k + res_bytes + B * Hq * D * 4 + B * Hq * L * 4
     alg_v = phys_v + res_bytes + B * Hq * L * 4 + B * Hq * D * 4
 
+    # HBM held by the compressed layer (SPEC.md:499 reports peak allocation): the arena's
+    # used bytes, its reserved capacity and the tables / staging next to fp16 K+V
+    tail = int(ls.tail.item())
+    side = sum(t.numel() * t.element_size() for t in (ls.blk_off, ls.blk_len, ls.perm, ls.nblk, ls.nres, ls.stage))
+    mem = {"fp16_kv_bytes": 2 * logical_kind, "arena_used_bytes": tail, "arena_capacity_bytes": ls.capacity,
+           "tables_and_staging_bytes": side, "hbm_ratio_vs_fp16": round(2 * logical_kind / (tail + side), 3),
+           "peak_allocated_bytes_after_build": int(torch.cuda.max_memory_allocated()),
+           "note": "arena capacity is geometric-growth reservation; CompressedStore.shrink_to_fit() releases it"}
     q = torch.randn((B, Hq, D), device="cuda")
     scores = torch.empty((B, Hq, L), device="cuda")
     out = torch.empty((B, Hq, D), device="cuda")
@@ -525,6 +533,7 @@ def main():
                             "fused K + softmax + fused V (attention_sim.GraphedAttention), NCCL all-gather of "
                             "per-head outputs, D2H out",
                     "ms_per_step": round(e2e_ms, 5)},
+            "memory": mem,
             "gpu_launches": 3 * K,
             "clocks": sampler.summary(),
         }

@@ -229,6 +229,18 @@ class LayerStore:
         if check:
             N.raise_flags(int(self.err.item()), "stage_token")
 
+    def shrink_to_fit(self, headroom_bytes: int = 0):
+        """Reallocate the arena to its used bytes (+ headroom): geometric growth
+        leaves up to ~2x reserved; the next append grows it again if needed."""
+        used = int(self.tail.item())
+        cap = _round16(used + max(0, int(headroom_bytes)))
+        if cap + 16 < self.arena.numel():
+            arena = torch.empty(cap + 16, dtype=torch.uint8, device=self.arena.device)
+            arena[:used].copy_(self.arena[:used])
+            self.arena = arena
+            self._struct = None
+        self.tail_ub = used
+
     # -- introspection (synchronising; parity / debug) ----------------------------
     def tables(self):
         o = self.owner
@@ -350,6 +362,11 @@ class CompressedStore:
         ls = self[layer]
         ents = [e for e in ls.directory() if e.kind == kind and e.seq == seq]
         return ents + [ResidueHandle(layer, ls.nblk_h * self.block, ls.nres_h, seq)]
+
+    def shrink_to_fit(self, headroom_bytes: int = 0):
+        """Release the arena capacity reserved beyond the compressed bytes (every layer)."""
+        for ls in self.layer_stores:
+            ls.shrink_to_fit(headroom_bytes)
 
     def check_errors(self):
         for ls in self.layer_stores:

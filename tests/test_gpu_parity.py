@@ -641,3 +641,20 @@ def test_fused_many_heads_config_d_shape():
     for h in range(0, H, 7):
         _close(s[0, h], O.naive_k_scores(ref, 0, h, q[0, h]))
         _close(o[0, h], O.naive_v_output(ref, 0, h, w[0, h]))
+
+
+def test_store_shrink_to_fit_keeps_bytes_and_appends():
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(81)
+    H, D = 2, 128
+    kk, vv = _kv(rng, 400, H, D)
+    a, b = CS(1, H, D, max_tokens=64), CS(1, H, D)
+    a.compress_batch(0, kk[:300], vv[:300])
+    b.compress_batch(0, kk[:300], vv[:300])
+    cap0 = a[0].capacity
+    a.shrink_to_fit()
+    assert a[0].capacity <= cap0 and a[0].capacity >= int(a[0].tail.item())
+    assert a[0].stream_bytes(0) == b[0].stream_bytes(0)
+    a.compress_batch(0, kk[300:], vv[300:])
+    b.compress_batch(0, kk[300:], vv[300:])
+    assert a[0].stream_bytes(0) == b[0].stream_bytes(0)
