@@ -526,7 +526,8 @@ def main():
                         "fused_v_gbs_physical": round(alg_v / (v_ms * 1e-3) / 1e9, 1)},
             "roofline": {"bound": "hbm", "kernel": f"fused_{dom}", "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "algorithmic_bytes_per_launch": alg},
+                         "traffic": traffic, "algorithmic_bytes_per_launch": alg,
+                         "frac_vs_nominal_8000_gbs": round(achieved / 8000.0, 4)},
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": B * Hq * D * 4,
                     "d2h_bytes_per_step": world * B * Hq * D * 4,
                     "path": "sharding.ShardedDecoder.step (public API): H2D q shard, one CUDA-graph replay of "
