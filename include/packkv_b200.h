@@ -150,6 +150,9 @@ int pkv_stage_token(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t*
  * holding every head.                                                      */
 int pkv_compress_codes(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new, int32_t ntok,
                        int32_t staged, float rel_k, float rel_v, uint16_t* codes, float* params, void* stream);
+/* pkv_repack_plan also backs repacker.repack_greedy / repack_v_median
+ * over any 1..64 vectors (block), with a partial last
+ * group when block % pack_size != 0.                        */
 int pkv_repack_plan(const uint16_t* codes, int32_t nsets, int32_t batch, int32_t heads, int32_t head_dim,
                     int32_t block, int32_t pack_size, int32_t repack, uint8_t* perm, void* stream);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:

@@ -58,3 +58,16 @@ def test_oracle_pkks_round_trip(tmp_path):
     with pytest.raises(E.StoreFormatError):
         (tmp_path / "u").write_bytes((tmp_path / "s").read_bytes()[:-1])
         O.load_pkks(tmp_path / "u")
+
+
+def test_repacker_cost_model_host():
+    """The SPEC cost model (host arithmetic) against the oracle's."""
+    from paper_2512_24449_b200 import repacker as R
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        g = rng.integers(0, 1000, (int(rng.integers(1, 17)), int(rng.integers(1, 40))))
+        assert R.pack_cost(g) == O.pack_cost(g)
+    X = rng.integers(0, 50, (30, 7))
+    perm = rng.permutation(30)
+    assert R.plan_cost(X, perm, 8) == O.plan_cost(X, perm, 8)
+    assert R.pack_cost(np.array([[0, 5], [3, 1]])) == 50

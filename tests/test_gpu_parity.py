@@ -658,3 +658,35 @@ def test_store_shrink_to_fit_keeps_bytes_and_appends():
     a.compress_batch(0, kk[300:], vv[300:])
     b.compress_batch(0, kk[300:], vv[300:])
     assert a[0].stream_bytes(0) == b[0].stream_bytes(0)
+
+
+# ------------------------------------------------------------------ repacker
+def test_repacker_spec_examples():
+    """SPEC.md:196,205,214-216 through the GPU plan kernel."""
+    from paper_2512_24449_b200 import repacker as R
+    assert R.pack_cost(np.array([[0, 5], [3, 1]])) == 50
+    p = R.repack_greedy(np.array([[0], [9], [0], [9]]), 2)
+    assert p.cost_bits == 40 and sorted(p.permutation.tolist()) == [0, 1, 2, 3]
+    v = np.array([[5], [1], [3]])
+    assert R.repack_v_median(v, v, 2).permutation.tolist() == [1, 2, 0]
+    v = np.array([[2], [2], [1]])
+    assert R.repack_v_median(v, v, 2).permutation.tolist() == [2, 0, 1]
+    assert R.repack_none(v, 2).permutation.tolist() == [0, 1, 2]
+
+
+@pytest.mark.parametrize("n,d,k", [(8, 6, 4), (37, 50, 8), (64, 256, 16), (64, 2048, 16), (20, 9, 16), (5, 3, 2)])
+def test_repacker_matches_oracle(n, d, k):
+    """Greedy and v_median plans (permutation and cost) equal the oracle's, partial
+    last groups and K+V vectors longer than one kernel head included."""
+    from paper_2512_24449_b200 import repacker as R
+    rng = np.random.default_rng(n * 1000 + d + k)
+    X = rng.integers(0, 12, (n, d)) + (rng.integers(0, 3, (n, 1)) * 7)
+    g = R.repack_greedy(X, k)
+    og = O.repack_greedy(X, k)
+    assert g.permutation.tolist() == og.permutation.tolist()
+    assert g.cost_bits == og.cost_bits
+    vp = X[:, d // 2:]
+    m = R.repack_v_median(X, vp, k)
+    om = O.repack_v_median(X, vp, k)
+    assert m.permutation.tolist() == om.permutation.tolist() and m.cost_bits == om.cost_bits
+    assert R.plan_cost(X, g.permutation, k) <= R.plan_cost(X, np.arange(n), k) or n <= k
