@@ -212,3 +212,41 @@ def attention_reference(K, V, q) -> torch.Tensor:
     if K.shape != V.shape or K.shape[1] != q.shape[0]:
         raise E.ShapeMismatchError("K, V, q dimensions disagree")
     return torch.softmax(K @ q / math.sqrt(K.shape[1]), 0) @ V
+
+
+def permutation_invariance_check(K, V, q, trials: int = 10, seed: int = 0, rel_scale_k: float = 0.1,
+                                 rel_scale_v: float = 0.2) -> dict:
+    """SPEC.md:537-545 (failures reported, not thrown).  K, V: [T, D] (one head),
+    q: [D].  (1) f64 attention under `trials` random joint permutations of the
+    rows against the unpermuted result (<= 1e-5 * |out|); (2) the compressed
+    path (device store, fused attention) with repacking greedy / v_median
+    against none (within 1e-4 relative)."""
+    import numpy as np
+    Kt = torch.as_tensor(np.asarray(K, dtype=np.float16) if not isinstance(K, torch.Tensor) else K)
+    Vt = torch.as_tensor(np.asarray(V, dtype=np.float16) if not isinstance(V, torch.Tensor) else V)
+    qt = torch.as_tensor(q).double()
+    if Kt.dim() != 2 or Kt.shape != Vt.shape or qt.shape != (Kt.shape[1],) or trials < 1:
+        raise E.ShapeMismatchError("K, V must be [T, D] and q [D]; trials >= 1")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Kd, Vd, qd = Kt.to(dev), Vt.to(dev), qt.to(dev)
+    T, D = Kt.shape
+    ref = attention_reference(Kd, Vd, qd)
+    g = torch.Generator(device="cpu")
+    g.manual_seed(seed)
+    worst = 0.0
+    fails = 0
+    for _ in range(trials):
+        p = torch.randperm(T, generator=g).to(dev)
+        err = float((attention_reference(Kd[p], Vd[p], qd) - ref).abs().max() / ref.abs().max().clamp_min(1e-300))
+        worst = max(worst, err)
+        fails += err > 1e-5
+    outs = {}
+    for strategy in ("none", "greedy", "v_median"):
+        st = CompressedStore(1, 1, D, rel_scale_k=rel_scale_k, rel_scale_v=rel_scale_v, repack=strategy)
+        st.compress_batch(0, Kd[:, None, :], Vd[:, None, :])
+        outs[strategy] = attention_decode(st, 0, 0, qd.float()).double()
+    base = outs["none"]
+    rep = {s: float((o - base).abs().max() / base.abs().max().clamp_min(1e-300)) for s, o in outs.items() if s != "none"}
+    return {"trials": trials, "f64_max_rel_err": worst, "f64_failures": int(fails),
+            "repack_vs_none_max_rel": rep, "repack_pass": all(v <= 1e-4 for v in rep.values()),
+            "pass": fails == 0 and all(v <= 1e-4 for v in rep.values())}

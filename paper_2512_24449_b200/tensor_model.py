@@ -79,3 +79,45 @@ def gauss_outlier(shape, head_dim_axis: int = -1, n_outlier: int = 4, amp: float
             sub = x[tuple(idx)]                      # (..., D) view
             sub[..., ch.to(device)] = sign.to(device) * amp + sigma * sub[..., ch.to(device)]
     return x.to(torch.float16)
+
+
+SYNTH_MODES = ("uniform", "channel-banded", "token-scaled", "gauss-outlier")
+
+
+def generate_synthetic(mode: str, seed: int, layers: int, heads: int, head_dim: int, tokens: int,
+                       amplitude: float = 1.0, device="cuda"):
+    """SPEC.md:58-66: (K, V) fp16 [layers, heads, tokens, head_dim], generated in HBM
+    with torch's CUDA generator (same seed + profile => byte-identical output):
+
+    * uniform         U(-a, a);
+    * channel-banded  a per-(layer, head, channel) offset U(-4a, 4a) + 0.25a N(0, 1):
+                      adjacent tokens of a column are correlated (Fig. 4);
+    * token-scaled    per-token scale U(0.1, 2)a times N(0, 1);
+    * gauss-outlier   the bench distribution (gauss_outlier).
+    """
+    if mode not in SYNTH_MODES:
+        raise ValueError(f"unknown synthetic mode {mode!r}; one of {SYNTH_MODES}")
+    if min(layers, heads, head_dim) < 1 or tokens < 0:
+        raise ValueError("counts must be >= 1 (tokens >= 0)")
+    shape = (layers, heads, tokens, head_dim)
+    if mode == "gauss-outlier":
+        k = gauss_outlier((layers, tokens, heads, head_dim), n_outlier=max(1, head_dim * 4 // 128), seed=seed,
+                          device=device, heads_axis=-2)
+        v = gauss_outlier((layers, tokens, heads, head_dim), n_outlier=max(1, head_dim // 128), seed=seed + 7,
+                          device=device, heads_axis=-2)
+        return k.permute(0, 2, 1, 3).contiguous(), v.permute(0, 2, 1, 3).contiguous()
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    a = float(amplitude)
+    out = []
+    for _ in range(2):
+        if mode == "uniform":
+            x = (torch.rand(shape, generator=g, device=device) * 2 - 1) * a
+        elif mode == "channel-banded":
+            off = (torch.rand((layers, heads, 1, head_dim), generator=g, device=device) * 8 - 4) * a
+            x = off + 0.25 * a * torch.randn(shape, generator=g, device=device)
+        else:
+            sc = (0.1 + 1.9 * torch.rand((layers, heads, tokens, 1), generator=g, device=device)) * a
+            x = sc * torch.randn(shape, generator=g, device=device)
+        out.append(x.to(torch.float16))
+    return out[0], out[1]

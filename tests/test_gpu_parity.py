@@ -690,3 +690,32 @@ def test_repacker_matches_oracle(n, d, k):
     om = O.repack_v_median(X, vp, k)
     assert m.permutation.tolist() == om.permutation.tolist() and m.cost_bits == om.cost_bits
     assert R.plan_cost(X, g.permutation, k) <= R.plan_cost(X, np.arange(n), k) or n <= k
+
+
+def test_generate_synthetic_profiles():
+    """determinism per seed; channel-banded packs have smaller
+    per-pack code ranges than uniform at equal amplitude."""
+    from paper_2512_24449_b200 import tensor_model as TM
+    from paper_2512_24449_b200.quantizer import quantize_token_wise
+    for mode in TM.SYNTH_MODES:
+        k1, v1 = TM.generate_synthetic(mode, 7, 2, 3, 128, 64)
+        k2, v2 = TM.generate_synthetic(mode, 7, 2, 3, 128, 64)
+        assert k1.shape == (2, 3, 64, 128) and torch.equal(k1, k2) and torch.equal(v1, v2)
+        assert torch.isfinite(k1.float()).all()
+    ranges = {}
+    for mode in ("uniform", "channel-banded"):
+        k, _ = TM.generate_synthetic(mode, 3, 1, 4, 128, 128)
+        q = quantize_token_wise(k.reshape(-1, 64, 128), 0.1).q.long().reshape(-1, 16, 128)
+        ranges[mode] = float((q.max(1).values - q.min(1).values).float().mean())
+    assert ranges["channel-banded"] < ranges["uniform"]
+
+
+def test_permutation_invariance_check():
+    """SPEC.md:537-545 (+ repacking neutrality)."""
+    from paper_2512_24449_b200.attention_sim import permutation_invariance_check
+    rng = np.random.default_rng(91)
+    K = rng.standard_normal((64 * 3 + 5, 128)).astype(np.float16)
+    V = rng.standard_normal((64 * 3 + 5, 128)).astype(np.float16)
+    rep = permutation_invariance_check(K, V, rng.standard_normal(128), trials=20)
+    assert rep["pass"], rep
+    assert rep["f64_failures"] == 0
