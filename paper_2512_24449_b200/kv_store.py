@@ -229,6 +229,20 @@ class LayerStore:
         if check:
             N.raise_flags(int(self.err.item()), "stage_token")
 
+    def width_hist(self, kind: int) -> List[int]:
+        """Pack-width histogram (0..15) over the layer's blocks of one kind, read
+        from the width nibbles of the blocks in HBM (Fig. 3 analog)."""
+        o = self.owner
+        nb = self.nblk_h
+        if nb == 0:
+            return [0] * 16
+        P = (o.block // o.pack_size) * o.head_dim
+        offs = self.blk_off[kind, :, :nb].reshape(-1)
+        idx = offs[:, None] + 8 + torch.arange((P + 1) // 2, device=offs.device)[None, :]
+        nib = self.arena[idx.reshape(-1)].to(torch.int64)
+        w = torch.stack([nib & 15, nib >> 4], 1).reshape(offs.numel(), -1)[:, :P]
+        return [int(x) for x in torch.bincount(w.reshape(-1), minlength=16).cpu().tolist()]
+
     def shrink_to_fit(self, headroom_bytes: int = 0):
         """Reallocate the arena to its used bytes (+ headroom): geometric growth
         leaves up to ~2x reserved; the next append grows it again if needed."""
@@ -385,7 +399,7 @@ class CompressedStore:
                 nblocks = int(ln[kind].size)
                 logical = nblocks * self.block * self.head_dim * 2
                 res = ls.nres_h * self.batch * self.heads * self.head_dim * 2 if include_staging else 0
-                widths = None
+                widths = ls.width_hist(kind) if nblocks else [0] * 16
                 out[(ls.layer, kind)] = {
                     "blocks": nblocks, "bytes_physical": phys + res, "bytes_logical": logical + res,
                     "cr": (logical + res) / (phys + res) if phys + res else None, "width_hist": widths,

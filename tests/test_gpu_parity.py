@@ -719,3 +719,29 @@ def test_permutation_invariance_check():
     rep = permutation_invariance_check(K, V, rng.standard_normal(128), trials=20)
     assert rep["pass"], rep
     assert rep["f64_failures"] == 0
+
+
+def test_snapshot_stats_width_histogram():
+    """exact bytes, CR and the pack-width histogram per (layer, kind)."""
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(93)
+    H, D = 2, 128
+    kk, vv = _kv(rng, 64 * 3 + 10, H, D)
+    st = CS(1, H, D)
+    st.compress_batch(0, kk, vv)
+    ref = O.OracleStore(1, H, D)
+    ref.compress_batch(0, kk, vv)
+    stats = st.snapshot_stats()
+    for kind in (0, 1):
+        ents = [e for e in ref.directory if e.kind == kind]
+        hist = np.zeros(16, np.int64)
+        for e in ents:
+            b = ref.block_bytes(e)
+            P = 4 * 128
+            nib = np.frombuffer(b[8:8 + P // 2], np.uint8)
+            hist += np.bincount(np.stack([nib & 15, nib >> 4], 1).ravel(), minlength=16)
+        s = stats[(0, kind)]
+        assert s["width_hist"] == hist.tolist()
+        assert s["bytes_physical"] == sum(e.byte_len for e in ents) and s["blocks"] == len(ents)
+    empty = CS(1, H, D).snapshot_stats()
+    assert empty[(0, 0)]["cr"] is None and empty[(0, 0)]["width_hist"] == [0] * 16
