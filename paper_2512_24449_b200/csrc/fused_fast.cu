@@ -178,6 +178,9 @@ __device__ __forceinline__ void spread8(uint32_t x, const uint4& c, uint32_t mr,
 #ifndef PKV_W2PRED
 #define PKV_W2PRED 0
 #endif
+#ifndef PKV_LUTREG
+#define PKV_LUTREG 0
+#endif
 // Shared-memory operands of one pack: the 3 words covering its <= 64-bit
 // payload (payload starts at bit `bit` of the block, bit % 16 == 0) and the
 // width's table entry.  Issued one pack ahead of the arithmetic.
@@ -202,7 +205,20 @@ __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ l
   // extra bits fall outside the 16 fields
   r.w2 = ld32(p + 8);
 #endif
-  r.c = *(const uint4*)(lut + w16);  // (computing the constants instead measured slower)
+#if PKV_LUTREG
+  // the width constants from w in registers (7 ALU/FMA ops) instead of an
+  // LDS.128 per pack: the shared-memory data pipe, not the ALU, is the K
+  // kernel's busiest unit (l1tex ~83%; the table read is 4 of its wavefronts)
+  {
+    const uint32_t w = w16 >> 4;
+    const uint32_t mc = 0x100u >> w;         // 2^(8-w)
+    const uint32_t mc2 = imad(mc, mc, 0u);   // 2^(16-2w)
+    const uint32_t ma = imad(mc2 >> 8, mc2 >> 8, 0u);  // 2^(16-4w)
+    r.c = make_uint4(ma, mc2 << 16, mc, (0x01010101u << w) - 0x01010101u);
+  }
+#else
+  r.c = *(const uint4*)(lut + w16);
+#endif
   return r;
 }
 // r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
@@ -460,6 +476,12 @@ constexpr int kWK = 4;               // warps per CTA
 #ifndef PKV_DIAG_WAITCLK
 #define PKV_DIAG_WAITCLK 0
 #endif
+#ifndef PKV_DIAG_FEEDPARSE
+#define PKV_DIAG_FEEDPARSE 0
+#endif
+#ifndef PKV_DIAG_NOSTS
+#define PKV_DIAG_NOSTS 0
+#endif
 #ifndef PKV_RBK  // ring bytes / slots per K warp (-D overrides for tools/exp variants)
 #define PKV_RBK (10 * 1024)
 #endif
@@ -634,6 +656,13 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
 #if PKV_DIAG_FEEDONLY
     if (j < nbk && lane == 0) sbase[j] = __uint_as_float(ld32(blk));
     if (false) {
+#elif PKV_DIAG_FEEDPARSE
+    if (j < nbk) {
+      Chunk ch;
+      const bool fast = gblk == nullptr && parse_chunk(blk, lane, lane, ch);
+      if (lane == 0) sbase[j] = __uint_as_float(ch.bit + fast + ch.mn[3] + ch.nb.y);
+    }
+    if (false) {
 #else
     if (j < nbk) {
 #endif
@@ -641,6 +670,9 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
       const bool fast = gblk == nullptr && parse_chunk(blk, lane, lane, ch);
       if (fast) {
         // packs in pairs (two independent decode chains), loads one pair ahead
+#if PKV_DIAG_NOSTS
+        uint32_t dsum = 0;
+#endif
         uint32_t bit = ch.bit;
         uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
         PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
@@ -664,8 +696,12 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
           pack_decode(A, bitA, min_rep(ch.mn, i2), ra);
           pack_decode(B, bitB, min_rep(ch.mn, i2 + 1), rb);
 #endif
+#if PKV_DIAG_NOSTS
+          dsum ^= ra[0] ^ ra[1] ^ ra[2] ^ ra[3] ^ rb[0] ^ rb[1] ^ rb[2] ^ rb[3];
+#else
           *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
           *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
+#endif
           bit = nbit;
           wa = nwa;
           wb = nwb;
@@ -685,7 +721,11 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
         float* p0 = sbase + int64_t(tq) * sstride + j * kRows + tok(gi);  // rows 16g + tok(gi) (+8) of head tq
         float* p1 = p0 + 4 * sstride;                                     // head tq + 4
 #if PKV_DIAG_NOMMA
+#if PKV_DIAG_NOSTS
+        if (tq < G) p0[0] = __uint_as_float(dsum) + __uint_as_float(prm[0][0]);
+#else
         if (tq < G) p0[0] = __uint_as_float(ld32(tile_s + 16u * lane)) + __uint_as_float(prm[0][0]);
+#endif
 #else
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
