@@ -34,6 +34,9 @@
 // inside the same launch (never at the default rel 0.1 / 0.2).
 #include "pkv_common.cuh"
 
+#include <mutex>
+#include <vector>
+
 using namespace pkv;
 
 namespace {
@@ -1300,23 +1303,30 @@ constexpr size_t v_smem_bytes() { return 256 + kWV * kWarpSmemV; }
 // never larger, so every warp's range is resident for the whole launch)
 template <class K>
 int fast_grid(K kernel, int threads, size_t smem, int64_t work_warps, int wpc) {
+  // resident CTAs per device for each kernel instantiation, queried once
+  // (occupancy queries cost microseconds per call); thread-safe, per device
   struct Cap {
     const void* k;
-    int cap;
+    int dev, cap;
   };
-  static Cap caps[8];
-  static int ncaps = 0;
+  static std::mutex mu;
+  static std::vector<Cap> caps;
+  int dev = 0;
+  cudaGetDevice(&dev);
   int cap = 0;
-  for (int i = 0; i < ncaps; ++i)
-    if (caps[i].k == (const void*)kernel) cap = caps[i].cap;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Cap& c : caps)
+      if (c.k == (const void*)kernel && c.dev == dev) cap = c.cap;
+  }
   if (!cap) {
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
+    int nsm = 0, per = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
     cap = max(1, per) * nsm;
-    if (ncaps < 8) caps[ncaps++] = {(const void*)kernel, cap};
+    std::lock_guard<std::mutex> lock(mu);
+    caps.push_back({(const void*)kernel, dev, cap});
   }
   const int64_t want = (work_warps + wpc - 1) / wpc;
   return int(want < 1 ? 1 : (want < cap ? want : cap));
