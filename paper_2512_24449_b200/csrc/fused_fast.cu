@@ -184,6 +184,9 @@ __device__ __forceinline__ void spread8(uint32_t x, const uint4& c, uint32_t mr,
 #ifndef PKV_LUTREG
 #define PKV_LUTREG 0
 #endif
+#ifndef PKV_KREGC  // K kernel: width constants in registers (measured -3.5% time with the 5.9 KB ring)
+#define PKV_KREGC 1
+#endif
 // Shared-memory operands of one pack: the 3 words covering its <= 64-bit
 // payload (payload starts at bit `bit` of the block, bit % 16 == 0) and the
 // width's table entry.  Issued one pack ahead of the arithmetic.
@@ -191,7 +194,7 @@ struct PackLd {
   uint32_t w0, w1, w2;
   uint4 c;
 };
-template <class P>
+template <bool REGC = false, class P>
 __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ lut, uint32_t bit, uint32_t w16) {
   const P p = blk + ((bit >> 5) << 2);
   PackLd r;
@@ -208,20 +211,19 @@ __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ l
   // extra bits fall outside the 16 fields
   r.w2 = ld32(p + 8);
 #endif
-#if PKV_LUTREG
-  // the width constants from w in registers (7 ALU/FMA ops) instead of an
-  // LDS.128 per pack: the shared-memory data pipe, not the ALU, is the K
-  // kernel's busiest unit (l1tex ~83%; the table read is 4 of its wavefronts)
-  {
+  if (REGC || PKV_LUTREG) {
+    // the width constants from w in registers (7 ALU/FMA ops) instead of an
+    // LDS.128 per pack (4 wavefronts of the L1/shared data pipe, which runs at
+    // ~70% in the K kernel; the V kernel is closer to its ALU limit and keeps
+    // the table)
     const uint32_t w = w16 >> 4;
-    const uint32_t mc = 0x100u >> w;         // 2^(8-w)
-    const uint32_t mc2 = imad(mc, mc, 0u);   // 2^(16-2w)
-    const uint32_t ma = imad(mc2 >> 8, mc2 >> 8, 0u);  // 2^(16-4w)
+    const uint32_t mc = 0x100u >> w;                    // 2^(8-w)
+    const uint32_t mc2 = imad(mc, mc, 0u);              // 2^(16-2w)
+    const uint32_t ma = imad(mc2 >> 8, mc2 >> 8, 0u);   // 2^(16-4w)
     r.c = make_uint4(ma, mc2 << 16, mc, (0x01010101u << w) - 0x01010101u);
+  } else {
+    r.c = *(const uint4*)(lut + w16);
   }
-#else
-  r.c = *(const uint4*)(lut + w16);
-#endif
   return r;
 }
 // r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
@@ -486,7 +488,10 @@ constexpr int kWK = 4;               // warps per CTA
 #define PKV_DIAG_NOSTS 0
 #endif
 #ifndef PKV_RBK  // ring bytes / slots per K warp (-D overrides for tools/exp variants)
-#define PKV_RBK (10 * 1024)
+// 5.9 KB: 8 KB tile + ring fit 4 CTAs of 4 warps per SM (16 warps) and still
+// hold the largest fast-path block (1544 + 512 * 8 B); measured 67.3 us vs
+// 69.8 us for a 10 KB ring at 3 CTAs per SM (config B)
+#define PKV_RBK 5888
 #endif
 #ifndef PKV_NSK
 #define PKV_NSK 3
@@ -678,7 +683,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
 #endif
         uint32_t bit = ch.bit;
         uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
-        PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
+        PackLd A = pack_load<PKV_KREGC>(blk, lutb, bit, wa), B = pack_load<PKV_KREGC>(blk, lutb, bit + wa, wb);
 #pragma unroll
         for (int i2 = 0; i2 < 16; i2 += 2) {
           const uint32_t bitA = bit, bitB = bit + wa;
@@ -688,8 +693,8 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
           if (i2 < 14) {
             nwa = w16_of(ch.nb, i2 + 2);
             nwb = w16_of(ch.nb, i2 + 3);
-            nA = pack_load(blk, lutb, nbit, nwa);
-            nB = pack_load(blk, lutb, nbit + nwa, nwb);
+            nA = pack_load<PKV_KREGC>(blk, lutb, nbit, nwa);
+            nB = pack_load<PKV_KREGC>(blk, lutb, nbit + nwa, nwb);
           }
           uint32_t ra[4], rb[4];
 #if PKV_DIAG_NODECODE
