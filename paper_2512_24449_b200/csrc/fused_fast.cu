@@ -911,7 +911,13 @@ __device__ __forceinline__ float row_max(const float* __restrict__ kmax, const f
   return m;
 }
 constexpr int kWV = 4;
-constexpr int kRBV = 10 * 1024, kNSV = 3;
+#ifndef PKV_VMINB  // V: CTAs per SM the register allocation must allow
+#define PKV_VMINB 4
+#endif
+#ifndef PKV_RBV
+#define PKV_RBV (10 * 1024)
+#endif
+constexpr int kRBV = PKV_RBV, kNSV = 3;
 using FeedV = Feed<kRBV, kNSV>;
 constexpr size_t kWarpSmemV = (2048 + FeedV::bytes() + 127) / 128 * 128;
 
@@ -920,7 +926,7 @@ constexpr size_t kWarpSmemV = (2048 + FeedV::bytes() + 127) / 128 * 128;
 // the K launch's statistics (kmax over its kslots warp slots, kres), so no
 // rescaling is ever needed, and each partial slot also carries l = sum p.
 template <int NT, bool SM>  // NT: n-tiles, 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kWV * 32, 4) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
+__global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
                                                                  int64_t wstride, float* __restrict__ part, int NB,
                                                                  int64_t total, int maxseg,
                                                                  float* __restrict__ vscr,
