@@ -535,6 +535,9 @@ def main():
                             "per-head outputs, D2H out",
                     "ms_per_step": round(e2e_ms, 5)},
             "memory": mem,
+            # scaling with and without the all-gather -- the same
+            # whole-job metric from the K + V launch times alone (max over ranks)
+            "value_without_collective": round(world * 2 * logical_kind / ((k_ms + v_ms) * 1e-3) / 1e9, 2),
             "gpu_launches": 3 * K,
             "clocks": sampler.summary(),
         }
