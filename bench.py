@@ -287,11 +287,11 @@ def compressor_bench(cfg, rank, T=4096, appends=128):
     res = {"prefill_tokens": B * T, "prefill_ms": round(pre_ms, 3),
            "prefill_tokens_per_s": round(B * T / (pre_ms * 1e-3)),
            "prefill_fp16_in_gbs": round(fp16_in / (pre_ms * 1e-3) / 1e9, 1),
-           # HBM traffic of the warp-per-block compressor: the f16 input is read by the
-           # width pass and again by the encode pass, the packed blocks written once
-           "prefill_hbm_gbs": round((2 * fp16_in + packed) / (pre_ms * 1e-3) / 1e9, 1),
-           "prefill_hbm_frac": round((2 * fp16_in + packed) / (pre_ms * 1e-3) / 1e9 / load_peaks()[0], 3),
-           "prefill_bound": "issue (f32 quantization twice + bit-packing per element), not HBM",
+           # HBM traffic of the single-pass compressor: the f16 input read once, the
+           # packed blocks written once
+           "prefill_hbm_gbs": round((fp16_in + packed) / (pre_ms * 1e-3) / 1e9, 1),
+           "prefill_hbm_frac": round((fp16_in + packed) / (pre_ms * 1e-3) / 1e9 / load_peaks()[0], 3),
+           "prefill_bound": "issue (f32 quantization + bit-packing per element), not HBM",
            "append_us_per_token": round(app_ms * 1e3 / appends, 2),
            "decode_step_us": round(step_ms * 1e3 / (appends - 1), 2),
            "decode_step_captures": dstep.captures - 1,
