@@ -321,15 +321,24 @@ __device__ __forceinline__ void build_desc(const Chunk& ch, int lane, uint32_t* 
 struct Range {
   int64_t b0, b1;
 };
+// With more warps than blocks (small layers: the grid is a whole number of
+// CTAs), warp W takes block W and the surplus warps come last: an empty range
+// in the middle of a unit would leave a partial-sum / score-maximum slot that
+// no warp writes (found by tests/test_gpu_parity.py::test_randomized_*).
 __host__ __device__ __forceinline__ Range warp_range(int64_t total, int64_t wid, int64_t nwarps) {
   Range r;
-  r.b0 = total * wid / nwarps;
-  r.b1 = total * (wid + 1) / nwarps;
+  if (nwarps > total) {
+    r.b0 = wid < total ? wid : total;
+    r.b1 = wid + 1 < total ? wid + 1 : total;
+  } else {
+    r.b0 = total * wid / nwarps;
+    r.b1 = total * (wid + 1) / nwarps;
+  }
   return r;
 }
 // the warp whose range contains block gb
 __host__ __device__ __forceinline__ int64_t warp_of(int64_t gb, int64_t total, int64_t nwarps) {
-  return ((gb + 1) * nwarps - 1) / total;
+  return nwarps > total ? gb : ((gb + 1) * nwarps - 1) / total;
 }
 
 // Position (unit u, block j) of a global block index, advanced without division.

@@ -745,3 +745,46 @@ def test_snapshot_stats_width_histogram():
         assert s["bytes_physical"] == sum(e.byte_len for e in ents) and s["blocks"] == len(ents)
     empty = CS(1, H, D).snapshot_stats()
     assert empty[(0, 0)]["cr"] is None and empty[(0, 0)]["width_hist"] == [0] * 16
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_randomized_end_to_end_parity(seed):
+    """Seeded random shapes / codec settings through the whole path: compressor
+    (split appends, repack strategy), streams bit-exact per sequence, fused K, V
+    and attention within the 1e-3 bar."""
+    _, _, F, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 4))
+    H = int(rng.integers(1, 5))
+    G = int(rng.choice([1, 2, 4, 8]))
+    T = int(rng.integers(1, 64 * 5))
+    rel_k = float(rng.choice([0.05, 0.1, 0.2]))
+    rel_v = float(rng.choice([0.1, 0.2, 0.3]))
+    repack = str(rng.choice(["none", "v_median", "greedy"]))
+    D = 128
+    kk = (rng.standard_normal((B, T, H, D)) * rng.uniform(0.2, 5, (B, T, 1, 1))).astype(np.float16)
+    vv = rng.standard_normal((B, T, H, D)).astype(np.float16)
+    st = CS(1, H, D, batch=B, rel_scale_k=rel_k, rel_scale_v=rel_v, repack=repack)
+    cut = int(rng.integers(0, T + 1))
+    st.compress_batch(0, kk[:, :cut], vv[:, :cut])
+    for t in range(cut, min(T, cut + 3)):
+        st.append_token(0, kk[:, t], vv[:, t])
+    if cut + 3 < T:
+        st.compress_batch(0, kk[:, cut + 3:], vv[:, cut + 3:])
+    q = rng.standard_normal((B, H * G, D)).astype(np.float32)
+    w = rng.random((B, H * G, T)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+    a = attention_decode_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    for b in range(B):
+        ref = O.OracleStore(1, H, D, rel_k=rel_k, rel_v=rel_v, repack=repack)
+        ref.compress_batch(0, kk[b], vv[b])
+        assert st[0].stream_bytes(b) == ref.layer_stream(0)
+        for hq in range(H * G):
+            rs = O.naive_k_scores(ref, 0, hq // G, q[b, hq])
+            _close(s[b, hq], rs)
+            _close(o[b, hq], O.naive_v_output(ref, 0, hq // G, w[b, hq]))
+            x = rs / np.sqrt(D)
+            p = np.exp(x - x.max())
+            _close(a[b, hq], O.naive_v_output(ref, 0, hq // G, p / p.sum()))
