@@ -55,7 +55,7 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
         return out
     s = fused_k_scores_batched(store, layer, q)
     a = torch.softmax(s, dim=-1)
-    return fused_v_output_batched(store, layer, a)
+    return fused_v_output_batched(store, layer, a, out=out)
 
 
 class _Captured:
@@ -88,6 +88,16 @@ class _Captured:
 
     def _attend(self, q: torch.Tensor) -> torch.Tensor:
         return attention_decode_batched(self.store, self.layer, q, scores=self._scores, out=self._out)
+
+    def _graphable(self, q: torch.Tensor) -> bool:
+        """Only the default format's folded-softmax launches (pkv_attention_decode)
+        read the residue length from the device; the generic composition (fused
+        K -> softmax -> fused V) bakes the host token count into its shapes, so it
+        runs eagerly."""
+        ls = self.store[self.layer]
+        if q.dim() != 3:
+            return False
+        return int(N.lib().pkv_attention_scratch_bytes(ctypes_ref(ls.struct()), ls.nblk_h, int(q.shape[1]))) > 0
 
     def _capture(self, record):
         """record() enqueues the step's launches; warmed up eagerly by the caller.
@@ -124,6 +134,8 @@ class GraphedAttention(_Captured):
 
     def __call__(self, q: torch.Tensor) -> torch.Tensor:
         q = _as_f32(q, self.store.device)
+        if not self._graphable(q):
+            return attention_decode_batched(self.store, self.layer, q)
         key = self._state(q)
         if key != self._key:
             self._q = q.clone()
@@ -148,6 +160,9 @@ class GraphedDecodeStep(_Captured):
     def __call__(self, k_tok, v_tok, q: torch.Tensor) -> torch.Tensor:
         st, ls = self.store, self.store[self.layer]
         q = _as_f32(q, st.device)
+        if not self._graphable(q):  # generic formats: eager append + composition
+            st.append_token(self.layer, k_tok, v_tok)
+            return attention_decode_batched(st, self.layer, q)
         if ls.nres_h + 1 >= st.block:  # block completes: eager compress + attention
             st.append_token(self.layer, k_tok, v_tok)
             self._buffers(q)

@@ -788,3 +788,46 @@ def test_randomized_end_to_end_parity(seed):
             x = rs / np.sqrt(D)
             p = np.exp(x - x.max())
             _close(a[b, hq], O.naive_v_output(ref, 0, hq // G, p / p.sum()))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_randomized_generic_formats_parity(seed):
+    """Seeded random pack sizes / head dims (the generic kernels) and the default
+    format, with a decode loop through GraphedDecodeStep: streams bit-exact,
+    fused K, V and attention within the 1e-3 bar."""
+    _, _, F, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeStep, attention_decode_batched
+    rng = np.random.default_rng(5000 + seed)
+    k = int(rng.choice([2, 4, 8, 16, 32]))
+    D = int(rng.choice([64, 128, 256]))
+    B = int(rng.integers(1, 3))
+    H = int(rng.integers(1, 4))
+    G = int(rng.choice([1, 2, 4]))
+    T = int(rng.integers(1, 64 * 3))
+    repack = str(rng.choice(["none", "v_median"]))
+    kk = (rng.standard_normal((B, T, H, D)) * rng.uniform(0.2, 3, (B, T, 1, 1))).astype(np.float16)
+    vv = rng.standard_normal((B, T, H, D)).astype(np.float16)
+    st = CS(1, H, D, batch=B, pack_size=k, repack=repack)
+    t0 = int(rng.integers(0, T + 1))
+    st.compress_batch(0, kk[:, :t0], vv[:, :t0])
+    step = GraphedDecodeStep(st, 0)
+    q = rng.standard_normal((B, H * G, D)).astype(np.float32)
+    for t in range(t0, T):  # decode steps: append token t, attend
+        out = step(torch.from_numpy(kk[:, t]).cuda(), torch.from_numpy(vv[:, t]).cuda(), torch.from_numpy(q).cuda())
+    if t0 == T:
+        out = attention_decode_batched(st, 0, torch.from_numpy(q))
+    out = out.cpu().numpy()
+    w = rng.random((B, H * G, T)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+    for b in range(B):
+        ref = O.OracleStore(1, H, D, pack_size=k, repack=repack)
+        ref.compress_batch(0, kk[b], vv[b])
+        assert st[0].stream_bytes(b) == ref.layer_stream(0)
+        for hq in range(H * G):
+            rs = O.naive_k_scores(ref, 0, hq // G, q[b, hq])
+            _close(s[b, hq], rs)
+            _close(o[b, hq], O.naive_v_output(ref, 0, hq // G, w[b, hq]))
+            x = rs / np.sqrt(D)
+            p = np.exp(x - x.max())
+            _close(out[b, hq], O.naive_v_output(ref, 0, hq // G, p / p.sum()))
