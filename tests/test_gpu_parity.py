@@ -831,3 +831,54 @@ def test_randomized_generic_formats_parity(seed):
             x = rs / np.sqrt(D)
             p = np.exp(x - x.max())
             _close(out[b, hq], O.naive_v_output(ref, 0, hq // G, p / p.sum()))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_randomized_store_files_layers_and_shards(seed, tmp_path):
+    """Random multi-layer stores (formats, repack, batch): PKKS save -> load ->
+    save bit-exact and attention-identical; kv-head-split repacking through
+    simulated ranks equals the single store."""
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200 import sharding as S
+    from paper_2512_24449_b200.kv_store import load_store, save_store
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    rng = np.random.default_rng(9000 + seed)
+    k = int(rng.choice([8, 16]))
+    D = int(rng.choice([64, 128]))
+    B = int(rng.integers(1, 3))
+    H = int(rng.choice([2, 4]))
+    layers = int(rng.integers(1, 3))
+    repack = str(rng.choice(["none", "v_median", "greedy"]))
+    st = CS(layers, H, D, batch=B, pack_size=k, repack=repack)
+    data = []
+    for layer in range(layers):
+        T = int(rng.integers(1, 64 * 3))
+        kk, vv = _kv(rng, T, H, D, batch=B)
+        data.append((kk, vv))
+        c = int(rng.integers(0, T + 1))
+        st.compress_batch(layer, kk[:, :c], vv[:, :c])
+        st.compress_batch(layer, kk[:, c:], vv[:, c:])
+    save_store(st, tmp_path / "a.pkks")
+    ld = load_store(tmp_path / "a.pkks")
+    save_store(ld, tmp_path / "b.pkks")
+    assert (tmp_path / "a.pkks").read_bytes() == (tmp_path / "b.pkks").read_bytes()
+    q = torch.from_numpy(rng.standard_normal((B, H * 2, D)).astype(np.float32)).cuda()
+    for layer in range(layers):
+        assert torch.equal(attention_decode_batched(ld, layer, q), attention_decode_batched(st, layer, q))
+    # shards of layer 0 (kv-head split over 2 simulated ranks)
+    kk, vv = data[0]
+    parts = [S.plan_partition(B, H, 2, r, prefer="head") for r in range(2)]
+    local = [CS(1, p.local_heads, D, batch=B, pack_size=k, repack=repack) for p in parts]
+    ks = [np.ascontiguousarray(kk[:, :, p.h0:p.h1]) for p in parts]
+    vs = [np.ascontiguousarray(vv[:, :, p.h0:p.h1]) for p in parts]
+    codes = []
+    for lst, k1, v1 in zip(local, ks, vs):
+        c = lst[0].pending_codes(lst._norm(k1, True), lst._norm(v1, True))
+        codes.append(None if c is None else c.view(torch.uint8))
+    for lst, p, k1, v1 in zip(local, parts, ks, vs):
+        S.compress_sharded(lst, p, 0, k1, v1, all_gather=lambda t: torch.stack(codes))
+    full = {(e.seq, e.kind, e.head, e.token_start): e for e in st[0].directory()}
+    for lst, p in zip(local, parts):
+        for e in lst[0].directory():
+            g = full[(e.seq, e.kind, e.head + p.h0, e.token_start)]
+            assert lst[0].block_bytes(e) == st[0].block_bytes(g)
