@@ -882,3 +882,35 @@ def test_randomized_store_files_layers_and_shards(seed, tmp_path):
         for e in lst[0].directory():
             g = full[(e.seq, e.kind, e.head + p.h0, e.token_start)]
             assert lst[0].block_bytes(e) == st[0].block_bytes(g)
+
+
+@pytest.mark.parametrize("G", [4, 8])
+def test_fused_normal_regime_parity(G):
+    """More blocks per kind than the grid has warps (ranges of 1-2 blocks that
+    straddle unit boundaries, the regime the benchmarks run in): fused K, V and
+    attention against the oracle on two sequences of a B = 8, H = 8 store."""
+    _, _, F, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    rng = np.random.default_rng(77 + G)
+    B, H, D, T = 8, 8, 128, 64 * 32 + 17
+    kk = (rng.standard_normal((B, T, H, D)) * rng.uniform(0.3, 3, (B, T, 1, 1))).astype(np.float16)
+    vv = rng.standard_normal((B, T, H, D)).astype(np.float16)
+    st = CS(1, H, D, batch=B)
+    st.compress_batch(0, kk, vv)
+    assert 2 * B * H * st[0].nblk_h > 2 * 1776
+    q = rng.standard_normal((B, H * G, D)).astype(np.float32)
+    w = rng.random((B, H * G, T)).astype(np.float32)
+    s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
+    a = attention_decode_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    for b in (0, 5):
+        ref = O.OracleStore(1, H, D)
+        ref.compress_batch(0, kk[b], vv[b])
+        assert st[0].stream_bytes(b) == ref.layer_stream(0)
+        for hq in range(0, H * G, 3):
+            rs = O.naive_k_scores(ref, 0, hq // G, q[b, hq])
+            _close(s[b, hq], rs)
+            _close(o[b, hq], O.naive_v_output(ref, 0, hq // G, w[b, hq]))
+            x = rs / np.sqrt(D)
+            p = np.exp(x - x.max())
+            _close(a[b, hq], O.naive_v_output(ref, 0, hq // G, p / p.sum()))
