@@ -914,3 +914,69 @@ def test_fused_normal_regime_parity(G):
             x = rs / np.sqrt(D)
             p = np.exp(x - x.max())
             _close(a[b, hq], O.naive_v_output(ref, 0, hq // G, p / p.sum()))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_randomized_codec_and_quantizer(seed):
+    """Random shapes / widths / scales through quantize, encode, decode and
+    decode_pack_at against the oracle (bit-exact)."""
+    _, C, _, Q, _ = _pk()
+    rng = np.random.default_rng(3000 + seed)
+    k = int(rng.choice([2, 4, 8, 16, 32]))
+    rows = k * int(rng.integers(1, 9))
+    cols = int(rng.integers(1, 300))
+    layout = int(rng.integers(0, 2))
+    mag = float(10 ** rng.uniform(-3, 4))
+    x = (rng.standard_normal((3, rows, cols)) * mag).astype(np.float16)
+    x[0, 0] = x[0, 0, 0]  # a constant row
+    rel = float(rng.choice([0.01, 0.05, 0.1, 0.3, 1.0]))
+    qb = Q.quantize_token_wise(torch.from_numpy(x).cuda(), rel, layout)
+    for i in range(3):
+        r = O.quantize_token_wise(x[i], rel)
+        assert np.array_equal(qb.q[i].cpu().numpy().astype(np.int64), r.q)
+        assert np.array_equal(qb.scale[i].cpu().numpy(), r.scale) and np.array_equal(qb.zp[i].cpu().numpy(), r.zp)
+    try:
+        blocks = C.encode_blocks(qb, k, layout)
+    except Exception as e:  # wide ranges at tiny rel: the oracle must refuse too
+        with pytest.raises(type(e)):
+            O.encode_block(O.quantize_token_wise(x[1], rel), k, layout, layout)
+        return
+    for i in range(3):
+        r = O.quantize_token_wise(x[i], rel)
+        ref = O.encode_block(O.QuantBlock(r.q, r.scale, r.zp, layout), k, layout, layout)
+        assert blocks[i].to_bytes() == ref
+        assert C.compression_ratio(blocks[i]) == O.compression_ratio(ref)
+        d = C.decode_block(C.PackedBlock.from_bytes(ref))
+        assert np.array_equal(d.q.cpu().numpy().astype(np.int64), r.q)
+        P = (rows // k) * cols
+        for p in rng.integers(0, P, 3):
+            assert np.array_equal(C.decode_pack_at(blocks[i], int(p)).cpu().numpy().astype(np.int64),
+                                  O.decode_pack_at(ref, int(p)))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_randomized_graphed_decode_loop(seed):
+    """GraphedDecodeStep (default format) over random batch / heads / groups and
+    start lengths, across block completions: every step bit-identical to the eager
+    append + attention on a twin store."""
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeStep, attention_decode_batched
+    rng = np.random.default_rng(7000 + seed)
+    B, H, G = int(rng.integers(1, 4)), int(rng.integers(1, 5)), int(rng.choice([1, 2, 4, 8]))
+    T0, steps, D = int(rng.integers(0, 200)), int(rng.integers(1, 140)), 128
+    a, b = CS(1, H, D, batch=B), CS(1, H, D, batch=B)
+    if T0:
+        k0, v0 = _kv(rng, T0, H, D, batch=B)
+        a.compress_batch(0, k0, v0)
+        b.compress_batch(0, k0, v0)
+    step = GraphedDecodeStep(a, 0)
+    for t in range(steps):
+        kt = torch.from_numpy(rng.standard_normal((B, H, D)).astype(np.float16)).cuda()
+        vt = torch.from_numpy(rng.standard_normal((B, H, D)).astype(np.float16)).cuda()
+        q = torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32)).cuda()
+        got = step(kt, vt, q).clone()
+        b.append_token(0, kt, vt)
+        assert torch.equal(got, attention_decode_batched(b, 0, q)), f"step {t}"
+    assert a[0].nblk_h == b[0].nblk_h and a[0].nres_h == b[0].nres_h
+    for s in range(B):
+        assert a[0].stream_bytes(s) == b[0].stream_bytes(s)
