@@ -133,10 +133,16 @@ class GraphedAttention(_Captured):
     when the store grows)."""
 
     def __call__(self, q: torch.Tensor) -> torch.Tensor:
+        if (isinstance(q, torch.Tensor) and not q.is_cuda and self._key is not None and q.dtype == torch.float32
+                and tuple(q.shape) == tuple(self._q.shape) and self._state(self._q) == self._key):
+            # a host query (pinned for async) goes straight into the graph's input buffer
+            self._q.copy_(q, non_blocking=True)
+            self._graph.replay()
+            return self._out
         q = _as_f32(q, self.store.device)
-        if not self._graphable(q):
-            return attention_decode_batched(self.store, self.layer, q)
         key = self._state(q)
+        if key != self._key and not self._graphable(q):
+            return attention_decode_batched(self.store, self.layer, q)
         if key != self._key:
             self._q = q.clone()
             self._buffers(q)
@@ -160,9 +166,10 @@ class GraphedDecodeStep(_Captured):
     def __call__(self, k_tok, v_tok, q: torch.Tensor) -> torch.Tensor:
         st, ls = self.store, self.store[self.layer]
         q = _as_f32(q, st.device)
-        if not self._graphable(q):  # generic formats: eager append + composition
-            st.append_token(self.layer, k_tok, v_tok)
-            return attention_decode_batched(st, self.layer, q)
+        if self._key is None or self._key[0] != ls.nblk_h:
+            if not self._graphable(q):  # generic formats: eager append + composition
+                st.append_token(self.layer, k_tok, v_tok)
+                return attention_decode_batched(st, self.layer, q)
         if ls.nres_h + 1 >= st.block:  # block completes: eager compress + attention
             st.append_token(self.layer, k_tok, v_tok)
             self._buffers(q)

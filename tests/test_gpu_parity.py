@@ -406,6 +406,10 @@ def test_graphed_attention_matches_eager_and_recaptures():
         kn = rng.standard_normal((B, 40, H, D)).astype(np.float16)
         vn = rng.standard_normal((B, 40, H, D)).astype(np.float16)
         st.compress_batch(0, kn, vn)  # 200 -> 240 -> 280: residue and block counts change
+    # a host (pinned) query is copied straight into the graph's buffer
+    qh = torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32)).pin_memory()
+    ga(qh.cuda())
+    assert torch.equal(ga(qh).clone(), attention_decode_batched(st, 0, qh.cuda()))
     # single-token appends that only stage (280 -> 283, 4 blocks + 24..27
     # staged): the same graph replays, the kernels read the residue length
     # from the device
