@@ -372,6 +372,9 @@ struct Cursor {
 #ifndef PKV_KPF  // L2 prefetch distance for the small-ring (K) feed, in blocks
 #define PKV_KPF 2  // measured -1.5% on K (5.9 KB ring holds ~1 block); 0 for the V ring
 #endif
+#ifndef PKV_VPF  // the same for the V feed (11 KB ring)
+#define PKV_VPF 0
+#endif
 template <int RB, int NS>
 struct Feed {
   uint8_t* ring;
@@ -454,7 +457,7 @@ struct Feed {
     __syncwarp();
     head += skip + size;
     ++issued;
-    prefetch_ahead<(RB < 8192 ? PKV_KPF : 0)>(L, nk, lane);
+    prefetch_ahead<(RB < 8192 ? PKV_KPF : PKV_VPF)>(L, nk, lane);
     return true;
   }
   // L2 prefetch of the block PF positions past the newest issued one (PF = 0: off)
