@@ -5,16 +5,18 @@
 // equal-sized range of the layer's (unit, block) sequence, unit = (sequence,
 // kv-head).  Every warp is its own producer:
 //  * it streams its blocks with 1-D TMA bulk copies (cp.async.bulk + mbarrier
-//    complete_tx) into a private shared-memory byte ring, two blocks ahead
-//    (bulk copies issued by one warp are serviced one after another, so a
-//    single producer warp per CTA cannot feed HBM-rate decoding).
+//    complete_tx) into a private shared-memory byte ring (V: 11 KB, up to two
+//    blocks ahead; K: 5.9 KB so 4 CTAs fit per SM, plus an L2 bulk prefetch
+//    two blocks ahead).  Bulk copies issued by one warp are serviced one after
+//    another, so a single producer warp per CTA cannot feed HBM-rate decoding.
 //  * Lane l walks a run of physically consecutive packs (SPEC.md:330 payloads
 //    are contiguous in physical pack order), so one warp prefix scan of the
 //    width nibbles gives each lane its starting bit and the lane
 //    then advances by 16*w bits per pack — no per-pack descriptor table.
 //  * Unpack (pack size 16, width w <= 4): two funnel shifts extract the pack's
-//    64-bit payload, a 16-entry shared-memory table gives the width's shift
-//    multipliers and byte mask, and a three-level select tree places the 16
+//    64-bit payload, the width's shift multipliers and byte mask come from a
+//    16-entry shared-memory table (V) or registers (K), and a three-level
+//    select tree places the 16
 //    fields into 4 registers of 4 bytes with the pack minimum added, i.e. the
 //    exact uint8 codes (SPEC.md:120 q values).  Byte order within a pack:
 //    position m holds row tok(m) = m with bits 1 and 2 swapped.
