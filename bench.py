@@ -362,9 +362,22 @@ def main():
     import numpy as np
     import torch
     import torch.distributed as dist
+    # PKV_BENCH_BACKEND=gloo (structural test of the N > 1 path with several ranks on
+    # one device); production runs use NCCL, one rank per GPU
+    backend = os.environ.get("PKV_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def gather_into(dst, src):
+        if backend == "nccl":
+            dist.all_gather_into_tensor(dst, src)
+        else:
+            dist.all_gather(list(dst.view(world, *src.shape).unbind(0)), src)
     from paper_2512_24449_b200 import fused_kernels as F
     from paper_2512_24449_b200 import sharding as S
 
@@ -407,7 +420,7 @@ def main():
         F.fused_k_scores_batched(st, 0, q, out=scores)
         F.fused_v_output_batched(st, 0, w, out=out)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
+            gather_into(gathered, out)
 
     for _ in range(args.warmup):
         step()
@@ -445,7 +458,7 @@ def main():
             gv.replay()
             evs[i][2].record()
             if world > 1:
-                dist.all_gather_into_tensor(gathered, out)
+                gather_into(gathered, out)
         e_end.record()
         torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
