@@ -37,6 +37,7 @@
 #include "pkv_common.cuh"
 
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 using namespace pkv;
@@ -121,6 +122,11 @@ __device__ __forceinline__ uint32_t umulhi(uint32_t a, uint32_t b) {
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
+__device__ __forceinline__ uint32_t shf_r_clamp(uint32_t lo, uint32_t hi, uint32_t s) {
+  uint32_t d;
+  asm("shf.r.clamp.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
+  return d;
+}
 __device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_t s) {
   uint32_t d;
   asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
@@ -158,8 +164,8 @@ __device__ __forceinline__ const uint8_t* gptr(uint32_t a) { return (const uint8
 // byte mask (2^w - 1) * 0x01010101.  Entry w at lut + 16*w.
 __device__ __forceinline__ void init_lut(uint4* lut, int tid) {
   if (tid < 16) {
-    const uint32_t w = tid <= 4 ? tid : 4;
-    lut[tid] = make_uint4(1u << (16 - 4 * w), w ? 1u << (32 - 2 * w) : 0u, 1u << (8 - w),
+    const uint32_t w = tid <= 8 ? tid : 8;
+    lut[tid] = make_uint4(w <= 4 ? 1u << (16 - 4 * w) : 0u, w ? 1u << (32 - 2 * w) : 0u, 1u << (8 - w),
                           ((1u << w) - 1u) * 0x01010101u);
   }
 }
@@ -233,13 +239,45 @@ __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ l
   return r;
 }
 // r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
-__device__ __forceinline__ void pack_decode(const PackLd& L, uint32_t bit, uint32_t mr, uint32_t (&r)[4]) {
-  const uint32_t x0 = shf_r_wrap(L.w0, L.w1, bit);  // payload bits 0..31
-  const uint32_t x1 = shf_r_wrap(L.w1, L.w2, bit);  // payload bits 32..63
-  const uint32_t md = imad(L.c.x, L.c.x, 0u);       // 2^(32-8w)
-  const uint32_t xh = imad(x1, md, umulhi(x0, md));  // fields 8..15 = payload >> 8w
-  spread8(x0, L.c, mr, r[0], r[1]);
-  spread8(xh, L.c, mr, r[2], r[3]);
+// 4 fields of width w <= 8 at stride w in x -> 4 bytes (fields 0..3), masked,
+// plus mr: the same two-level select tree as spread8 with the 8w-bit halves.
+__device__ __forceinline__ uint32_t spread4(uint32_t x, uint32_t a2, uint32_t c, uint32_t mask, uint32_t mr) {
+  const uint32_t t = sel<0x0000ffffu>(x, imad(x, a2, 0u));  // fields 2,3 -> bit 16
+  const uint32_t u = sel<0x00ff00ffu>(t, imad(t, c, 0u));   // fields 1,3 -> bits 8, 24
+  return imad(u & mask, 1u, mr);
+}
+// r[0..3] = the 16 codes at byte positions 0..15 (see tok()).  WIDE (blocks
+// holding any pack of width 5..8, a warp-uniform choice): such packs (80..128
+// payload bits over up to 5 words) take a second path; codes stay bytes
+// because the block check guarantees min + 2^w - 1 <= 255.  Blocks without
+// wide packs run the narrow code only.
+template <bool WIDE, class P>
+__device__ __forceinline__ void pack_decode(P blk, const PackLd& L, uint32_t bit, uint32_t w16, uint32_t mr,
+                                            uint32_t (&r)[4]) {
+  if (!WIDE || w16 <= 64u) {
+    const uint32_t x0 = shf_r_wrap(L.w0, L.w1, bit);  // payload bits 0..31
+    const uint32_t x1 = shf_r_wrap(L.w1, L.w2, bit);  // payload bits 32..63
+    const uint32_t md = imad(L.c.x, L.c.x, 0u);       // 2^(32-8w)
+    const uint32_t xh = imad(x1, md, umulhi(x0, md));  // fields 8..15 = payload >> 8w
+    spread8(x0, L.c, mr, r[0], r[1]);
+    spread8(xh, L.c, mr, r[2], r[3]);
+  } else {
+    const P p = blk + ((bit >> 5) << 2);
+    const uint32_t w3 = ld32(p + 12), w4 = ld32(p + 16);
+    const uint32_t w = w16 >> 4;
+    const uint32_t y0 = shf_r_wrap(L.w0, L.w1, bit), y1 = shf_r_wrap(L.w1, L.w2, bit);
+    const uint32_t y2 = shf_r_wrap(L.w2, w3, bit), y3 = shf_r_wrap(w3, w4, bit);
+    // fields 8..15 start at payload bit 8w (40..64)
+    const uint32_t s1 = 8u * w - 32u;
+    const uint32_t z0 = w == 8u ? y2 : shf_r_wrap(y1, y2, s1), z1 = w == 8u ? y3 : shf_r_wrap(y2, y3, s1);
+    const uint32_t a2 = imad(L.c.z, L.c.z, 0u);  // 2^(16-2w)
+    const uint32_t q0 = spread4(y0, a2, L.c.z, L.c.w, mr), q1 = spread4(shf_r_clamp(y0, y1, 4u * w), a2, L.c.z, L.c.w, mr);
+    const uint32_t q2 = spread4(z0, a2, L.c.z, L.c.w, mr), q3 = spread4(shf_r_clamp(z0, z1, 4u * w), a2, L.c.z, L.c.w, mr);
+    r[0] = __byte_perm(q0, q1, 0x5410u);  // fields 0, 1, 4, 5
+    r[1] = __byte_perm(q0, q1, 0x7632u);  // fields 2, 3, 6, 7
+    r[2] = __byte_perm(q2, q3, 0x5410u);
+    r[3] = __byte_perm(q2, q3, 0x7632u);
+  }
 }
 // width of pack i of a lane's 16 (nibbles nb), times 16
 __device__ __forceinline__ uint32_t w16_of(const uint2& nb, int i) {
@@ -274,6 +312,7 @@ struct Chunk {
   uint2 nb;       // 16 width nibbles
   uint32_t mn[8]; // 16 u16 minima
   uint32_t bit;   // payload bit offset of the chunk's first pack
+  bool wide;      // the block has a pack of width 5..8 (warp-uniform)
 };
 template <class P>
 __device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& ch) {
@@ -288,9 +327,14 @@ __device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& 
 #pragma unroll
   for (int q = 0; q < 8; ++q) mor |= ch.mn[q];
   const uint32_t nx = ch.nb.x, ny = ch.nb.y;
-  const uint32_t bad = ((nx | ny) & 0x88888888u) |
-                       (((nx >> 2) & (nx | (nx >> 1))) & 0x11111111u) | (((ny >> 2) & (ny | (ny >> 1))) & 0x11111111u);
-  const bool ok = bad == 0 && ((mor | (mor >> 16)) & 0xffffu) <= 240u;
+  // w <= 4 everywhere and minima <= 240, or w <= 7 and minima <= 128: every
+  // code min + 2^w - 1 fits a byte (w = 8 packs and larger minima: scalar path)
+  const uint32_t ge8 = (nx | ny) & 0x88888888u;
+  const uint32_t ge5 = (((nx >> 2) & (nx | (nx >> 1))) & 0x11111111u) | (((ny >> 2) & (ny | (ny >> 1))) & 0x11111111u);
+  // (warp-wide: in V a lane checks the widths of one chunk and the minima of another)
+  const uint32_t mo = (mor | (mor >> 16)) & 0xffffu;
+  ch.wide = __any_sync(PKV_FULL, ge5 != 0u);
+  const bool ok = ge8 == 0 && mo <= (ch.wide ? 128u : 240u);
   uint32_t a = (nx & 0x0f0f0f0fu) + ((nx >> 4) & 0x0f0f0f0fu) + (ny & 0x0f0f0f0fu) + ((ny >> 4) & 0x0f0f0f0fu);
   a = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu);
   const uint32_t lsum = 16u * ((a & 0xffffu) + (a >> 16));  // payload bits (k = 16)
@@ -713,43 +757,48 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
 #if PKV_DIAG_NOSTS
         uint32_t dsum = 0;
 #endif
-        uint32_t bit = ch.bit;
-        uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
-        PackLd A = pack_load<PKV_KREGC>(blk, lutb, bit, wa), B = pack_load<PKV_KREGC>(blk, lutb, bit + wa, wb);
-#pragma unroll
-        for (int i2 = 0; i2 < 16; i2 += 2) {
-          const uint32_t bitA = bit, bitB = bit + wa;
-          const uint32_t nbit = bitB + wb;
-          uint32_t nwa = 0, nwb = 0;
-          PackLd nA, nB;
-          if (i2 < 14) {
-            nwa = w16_of(ch.nb, i2 + 2);
-            nwb = w16_of(ch.nb, i2 + 3);
-            nA = pack_load<PKV_KREGC>(blk, lutb, nbit, nwa);
-            nB = pack_load<PKV_KREGC>(blk, lutb, nbit + nwa, nwb);
+        // the narrow-only loop unless the block holds a pack of width 5..8
+        auto decode_packs = [&](auto wide) {
+          uint32_t bit = ch.bit;
+          uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
+          PackLd A = pack_load<PKV_KREGC>(blk, lutb, bit, wa), B = pack_load<PKV_KREGC>(blk, lutb, bit + wa, wb);
+  #pragma unroll
+          for (int i2 = 0; i2 < 16; i2 += 2) {
+            const uint32_t bitA = bit, bitB = bit + wa;
+            const uint32_t nbit = bitB + wb;
+            uint32_t nwa = 0, nwb = 0;
+            PackLd nA, nB;
+            if (i2 < 14) {
+              nwa = w16_of(ch.nb, i2 + 2);
+              nwb = w16_of(ch.nb, i2 + 3);
+              nA = pack_load<PKV_KREGC>(blk, lutb, nbit, nwa);
+              nB = pack_load<PKV_KREGC>(blk, lutb, nbit + nwa, nwb);
+            }
+            uint32_t ra[4], rb[4];
+  #if PKV_DIAG_NODECODE
+            ra[0] = A.w0 ^ bitA; ra[1] = A.w1; ra[2] = A.w2; ra[3] = A.c.x;
+            rb[0] = B.w0 ^ bitB; rb[1] = B.w1; rb[2] = B.w2; rb[3] = B.c.x;
+  #else
+            pack_decode<decltype(wide)::value>(blk, A, bitA, wa, min_rep(ch.mn, i2), ra);
+            pack_decode<decltype(wide)::value>(blk, B, bitB, wb, min_rep(ch.mn, i2 + 1), rb);
+  #endif
+  #if PKV_DIAG_NOSTS
+            dsum ^= ra[0] ^ ra[1] ^ ra[2] ^ ra[3] ^ rb[0] ^ rb[1] ^ rb[2] ^ rb[3];
+  #else
+            *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+            *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
+  #endif
+            bit = nbit;
+            wa = nwa;
+            wb = nwb;
+            if (i2 < 14) {
+              A = nA;
+              B = nB;
+            }
           }
-          uint32_t ra[4], rb[4];
-#if PKV_DIAG_NODECODE
-          ra[0] = A.w0 ^ bitA; ra[1] = A.w1; ra[2] = A.w2; ra[3] = A.c.x;
-          rb[0] = B.w0 ^ bitB; rb[1] = B.w1; rb[2] = B.w2; rb[3] = B.c.x;
-#else
-          pack_decode(A, bitA, min_rep(ch.mn, i2), ra);
-          pack_decode(B, bitB, min_rep(ch.mn, i2 + 1), rb);
-#endif
-#if PKV_DIAG_NOSTS
-          dsum ^= ra[0] ^ ra[1] ^ ra[2] ^ ra[3] ^ rb[0] ^ rb[1] ^ rb[2] ^ rb[3];
-#else
-          *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
-          *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
-#endif
-          bit = nbit;
-          wa = nwa;
-          wb = nwb;
-          if (i2 < 14) {
-            A = nA;
-            B = nB;
-          }
-        }
+        };
+        if (ch.wide) decode_packs(std::true_type{});
+        else decode_packs(std::false_type{});
         // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
         uint32_t prm[4][2];
 #pragma unroll
@@ -1145,44 +1194,48 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
         const uint2 nb = ld64(blk + kNib + 8 * src);
         const uint32_t (&mn)[8] = ch.mn;
         // the m-tile's two packs decoded together, the next pair's loads in flight
-        uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
-        PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          uint32_t P[2][4];
-          {
-            const int i2 = 2 * mt;
-            const uint32_t bitA = bit, bitB = bit + wa;
-            const uint32_t nbit = bitB + wb;
-            uint32_t nwa = 0, nwb = 0;
-            PackLd nA, nB;
-            if (i2 < 14) {
-              nwa = w16_of(nb, i2 + 2);
-              nwb = w16_of(nb, i2 + 3);
-              nA = pack_load(blk, lutb, nbit, nwa);
-              nB = pack_load(blk, lutb, nbit + nwa, nwb);
+        auto decode_mma = [&](auto wide) {
+          uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
+          PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
+  #pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            uint32_t P[2][4];
+            {
+              const int i2 = 2 * mt;
+              const uint32_t bitA = bit, bitB = bit + wa;
+              const uint32_t nbit = bitB + wb;
+              uint32_t nwa = 0, nwb = 0;
+              PackLd nA, nB;
+              if (i2 < 14) {
+                nwa = w16_of(nb, i2 + 2);
+                nwb = w16_of(nb, i2 + 3);
+                nA = pack_load(blk, lutb, nbit, nwa);
+                nB = pack_load(blk, lutb, nbit + nwa, nwb);
+              }
+              pack_decode<decltype(wide)::value>(blk, A, bitA, wa, min_rep(mn, i2), P[0]);
+              pack_decode<decltype(wide)::value>(blk, B, bitB, wb, min_rep(mn, i2 + 1), P[1]);
+              bit = nbit;
+              wa = nwa;
+              wb = nwb;
+              if (i2 < 14) {
+                A = nA;
+                B = nB;
+              }
             }
-            pack_decode(A, bitA, min_rep(mn, i2), P[0]);
-            pack_decode(B, bitB, min_rep(mn, i2 + 1), P[1]);
-            bit = nbit;
-            wa = nwa;
-            wb = nwb;
-            if (i2 < 14) {
-              A = nA;
-              B = nB;
+  #pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              int d[4] = {0, 0, 0, 0};
+              const uint32_t a0[4] = {P[0][0], P[1][0], P[0][1], P[1][1]};
+              imma_uu(d, a0, bf[nt][0], bf[nt][1]);
+              const uint32_t a1[4] = {P[0][2], P[1][2], P[0][3], P[1][3]};
+              imma_uu(d, a1, bf[nt][2], bf[nt][3]);
+              acc[nt][2 * mt] = fmaf(float(d[0] + 256 * d[1]), inv[nt], acc[nt][2 * mt]);
+              acc[nt][2 * mt + 1] = fmaf(float(d[2] + 256 * d[3]), inv[nt], acc[nt][2 * mt + 1]);
             }
           }
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            int d[4] = {0, 0, 0, 0};
-            const uint32_t a0[4] = {P[0][0], P[1][0], P[0][1], P[1][1]};
-            imma_uu(d, a0, bf[nt][0], bf[nt][1]);
-            const uint32_t a1[4] = {P[0][2], P[1][2], P[0][3], P[1][3]};
-            imma_uu(d, a1, bf[nt][2], bf[nt][3]);
-            acc[nt][2 * mt] = fmaf(float(d[0] + 256 * d[1]), inv[nt], acc[nt][2 * mt]);
-            acc[nt][2 * mt + 1] = fmaf(float(d[2] + 256 * d[3]), inv[nt], acc[nt][2 * mt + 1]);
-          }
-        }
+        };
+        if (ch.wide) decode_mma(std::true_type{});
+        else decode_mma(std::false_type{});
       } else {
         // scalar path (rare): lane owns channels lane + 32q, all 64 rows, all heads;
         // partials accumulate in this warp's global scratch (fixed order, deterministic)
