@@ -751,114 +751,124 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
     if (j < nbk) {
 #endif
       Chunk ch;
-      const bool fast = gblk == nullptr && parse_chunk(blk, lane, lane, ch);
-      if (fast) {
+      // the fast path on the staged copy, or in place (global loads) on a block
+      // too large for the ring
+      auto fast_block = [&](auto bp) {
         // packs in pairs (two independent decode chains), loads one pair ahead
-#if PKV_DIAG_NOSTS
-        uint32_t dsum = 0;
-#endif
-        // the narrow-only loop unless the block holds a pack of width 5..8
-        auto decode_packs = [&](auto wide) {
-          uint32_t bit = ch.bit;
-          uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
-          PackLd A = pack_load<PKV_KREGC>(blk, lutb, bit, wa), B = pack_load<PKV_KREGC>(blk, lutb, bit + wa, wb);
-  #pragma unroll
-          for (int i2 = 0; i2 < 16; i2 += 2) {
-            const uint32_t bitA = bit, bitB = bit + wa;
-            const uint32_t nbit = bitB + wb;
-            uint32_t nwa = 0, nwb = 0;
-            PackLd nA, nB;
-            if (i2 < 14) {
-              nwa = w16_of(ch.nb, i2 + 2);
-              nwb = w16_of(ch.nb, i2 + 3);
-              nA = pack_load<PKV_KREGC>(blk, lutb, nbit, nwa);
-              nB = pack_load<PKV_KREGC>(blk, lutb, nbit + nwa, nwb);
-            }
-            uint32_t ra[4], rb[4];
-  #if PKV_DIAG_NODECODE
-            ra[0] = A.w0 ^ bitA; ra[1] = A.w1; ra[2] = A.w2; ra[3] = A.c.x;
-            rb[0] = B.w0 ^ bitB; rb[1] = B.w1; rb[2] = B.w2; rb[3] = B.c.x;
-  #else
-            pack_decode<decltype(wide)::value>(blk, A, bitA, wa, min_rep(ch.mn, i2), ra);
-            pack_decode<decltype(wide)::value>(blk, B, bitB, wb, min_rep(ch.mn, i2 + 1), rb);
-  #endif
   #if PKV_DIAG_NOSTS
-            dsum ^= ra[0] ^ ra[1] ^ ra[2] ^ ra[3] ^ rb[0] ^ rb[1] ^ rb[2] ^ rb[3];
-  #else
-            *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
-            *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
+          uint32_t dsum = 0;
   #endif
-            bit = nbit;
-            wa = nwa;
-            wb = nwb;
-            if (i2 < 14) {
-              A = nA;
-              B = nB;
+          // the narrow-only loop unless the block holds a pack of width 5..8
+          auto decode_packs = [&](auto wide) {
+            uint32_t bit = ch.bit;
+            uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
+            PackLd A = pack_load<PKV_KREGC>(bp, lutb, bit, wa), B = pack_load<PKV_KREGC>(bp, lutb, bit + wa, wb);
+    #pragma unroll
+            for (int i2 = 0; i2 < 16; i2 += 2) {
+              const uint32_t bitA = bit, bitB = bit + wa;
+              const uint32_t nbit = bitB + wb;
+              uint32_t nwa = 0, nwb = 0;
+              PackLd nA, nB;
+              if (i2 < 14) {
+                nwa = w16_of(ch.nb, i2 + 2);
+                nwb = w16_of(ch.nb, i2 + 3);
+                nA = pack_load<PKV_KREGC>(bp, lutb, nbit, nwa);
+                nB = pack_load<PKV_KREGC>(bp, lutb, nbit + nwa, nwb);
+              }
+              uint32_t ra[4], rb[4];
+    #if PKV_DIAG_NODECODE
+              ra[0] = A.w0 ^ bitA; ra[1] = A.w1; ra[2] = A.w2; ra[3] = A.c.x;
+              rb[0] = B.w0 ^ bitB; rb[1] = B.w1; rb[2] = B.w2; rb[3] = B.c.x;
+    #else
+              pack_decode<decltype(wide)::value>(bp, A, bitA, wa, min_rep(ch.mn, i2), ra);
+              pack_decode<decltype(wide)::value>(bp, B, bitB, wb, min_rep(ch.mn, i2 + 1), rb);
+    #endif
+    #if PKV_DIAG_NOSTS
+              dsum ^= ra[0] ^ ra[1] ^ ra[2] ^ ra[3] ^ rb[0] ^ rb[1] ^ rb[2] ^ rb[3];
+    #else
+              *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+              *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
+    #endif
+              bit = nbit;
+              wa = nwa;
+              wb = nwb;
+              if (i2 < 14) {
+                A = nA;
+                B = nB;
+              }
+            }
+          };
+          if (ch.wide) decode_packs(std::true_type{});
+          else decode_packs(std::false_type{});
+          // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
+          uint32_t prm[4][2];
+  #pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            prm[g][0] = ld32(bp + kPar + 4 * (16 * g + tok(gi)));
+            prm[g][1] = ld32(bp + kPar + 4 * (16 * g + tok(gi) + 8));
+          }
+          __syncwarp();
+          float* p0 = sbase + int64_t(tq) * sstride + j * kRows + tok(gi);  // rows 16g + tok(gi) (+8) of head tq
+          float* p1 = p0 + 4 * sstride;                                     // head tq + 4
+  #if PKV_DIAG_NOMMA
+  #if PKV_DIAG_NOSTS
+          if (tq < G) p0[0] = __uint_as_float(dsum) + __uint_as_float(prm[0][0]);
+  #else
+          if (tq < G) p0[0] = __uint_as_float(ld32(tile_s + 16u * lane)) + __uint_as_float(prm[0][0]);
+  #endif
+  #else
+  #pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            int accU[NU][4], accS[4];
+  #pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              accS[e] = 0;
+  #pragma unroll
+              for (int nu = 0; nu < NU; ++nu) accU[nu][e] = 0;
+            }
+            // lane L addresses row R = 128g + 32jj + L
+            const uint32_t a0 = tile_s + 16u * (128u * g + lane);              // jj = 0, 1 (+512 B)
+            const uint32_t a1 = tile_s + 16u * (128u * g + (lane ^ 4u) + 64u);  // jj = 2, 3
+  #pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              uint32_t a[4];
+              ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
+  #pragma unroll
+              for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, Q.u[nu][jj][0], Q.u[nu][jj][1]);
+              imma_us(accS, a, Q.s[jj][0], Q.s[jj][1]);
+            }
+            const float sA = h2f(prm[g][0] & 0xffff), zA = h2f(prm[g][0] >> 16);
+            const float sB = h2f(prm[g][1] & 0xffff), zB = h2f(prm[g][1] >> 16);
+            // digit sums: d0 + 256*d1 <= 128*255*65535 < 2^31 is exact in int32
+            if (tq < G) {
+              const float vA = fmaf(65536.f, float(accS[0]), float(accU[0][0] + 256 * accU[0][1]));
+              const float vB = fmaf(65536.f, float(accS[2]), float(accU[0][2] + 256 * accU[0][3]));
+              const float scA = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]), scB = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
+              p0[16 * g] = scA;
+              p0[16 * g + 8] = scB;
+              if (ST) kmx0 = fmaxf(kmx0, fmaxf(scA, scB));
+            }
+            if (NU == 2 && tq + 4 < G) {
+              const float vA = fmaf(65536.f, float(accS[1]), float(accU[NU - 1][0] + 256 * accU[NU - 1][1]));
+              const float vB = fmaf(65536.f, float(accS[3]), float(accU[NU - 1][2] + 256 * accU[NU - 1][3]));
+              const float scA = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]), scB = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
+              p1[16 * g] = scA;
+              p1[16 * g + 8] = scB;
+              if (ST) kmx1 = fmaxf(kmx1, fmaxf(scA, scB));
             }
           }
-        };
-        if (ch.wide) decode_packs(std::true_type{});
-        else decode_packs(std::false_type{});
-        // (scale, zp) of the rows this lane finalises: 16g + tok(gi) (+8)
-        uint32_t prm[4][2];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          prm[g][0] = ld32(blk + kPar + 4 * (16 * g + tok(gi)));
-          prm[g][1] = ld32(blk + kPar + 4 * (16 * g + tok(gi) + 8));
-        }
-        __syncwarp();
-        float* p0 = sbase + int64_t(tq) * sstride + j * kRows + tok(gi);  // rows 16g + tok(gi) (+8) of head tq
-        float* p1 = p0 + 4 * sstride;                                     // head tq + 4
-#if PKV_DIAG_NOMMA
-#if PKV_DIAG_NOSTS
-        if (tq < G) p0[0] = __uint_as_float(dsum) + __uint_as_float(prm[0][0]);
-#else
-        if (tq < G) p0[0] = __uint_as_float(ld32(tile_s + 16u * lane)) + __uint_as_float(prm[0][0]);
-#endif
-#else
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          int accU[NU][4], accS[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            accS[e] = 0;
-#pragma unroll
-            for (int nu = 0; nu < NU; ++nu) accU[nu][e] = 0;
-          }
-          // lane L addresses row R = 128g + 32jj + L
-          const uint32_t a0 = tile_s + 16u * (128u * g + lane);              // jj = 0, 1 (+512 B)
-          const uint32_t a1 = tile_s + 16u * (128u * g + (lane ^ 4u) + 64u);  // jj = 2, 3
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            uint32_t a[4];
-            ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
-#pragma unroll
-            for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, Q.u[nu][jj][0], Q.u[nu][jj][1]);
-            imma_us(accS, a, Q.s[jj][0], Q.s[jj][1]);
-          }
-          const float sA = h2f(prm[g][0] & 0xffff), zA = h2f(prm[g][0] >> 16);
-          const float sB = h2f(prm[g][1] & 0xffff), zB = h2f(prm[g][1] >> 16);
-          // digit sums: d0 + 256*d1 <= 128*255*65535 < 2^31 is exact in int32
-          if (tq < G) {
-            const float vA = fmaf(65536.f, float(accS[0]), float(accU[0][0] + 256 * accU[0][1]));
-            const float vB = fmaf(65536.f, float(accS[2]), float(accU[0][2] + 256 * accU[0][3]));
-            const float scA = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]), scB = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
-            p0[16 * g] = scA;
-            p0[16 * g + 8] = scB;
-            if (ST) kmx0 = fmaxf(kmx0, fmaxf(scA, scB));
-          }
-          if (NU == 2 && tq + 4 < G) {
-            const float vA = fmaf(65536.f, float(accS[1]), float(accU[NU - 1][0] + 256 * accU[NU - 1][1]));
-            const float vB = fmaf(65536.f, float(accS[3]), float(accU[NU - 1][2] + 256 * accU[NU - 1][3]));
-            const float scA = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]), scB = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
-            p1[16 * g] = scA;
-            p1[16 * g + 8] = scB;
-            if (ST) kmx1 = fmaxf(kmx1, fmaxf(scA, scB));
-          }
-        }
-#endif
-        __syncwarp();  // tile reads done before the next block's stores
+  #endif
+          __syncwarp();  // tile reads done before the next block's stores
+      };
+      bool fast;
+      if (gblk == nullptr) {
+        fast = parse_chunk(blk, lane, lane, ch);
+        if (fast) fast_block(blk);
       } else {
+        fast = parse_chunk(gblk, lane, lane, ch);
+        if (fast) fast_block(gblk);
+      }
+      if (!fast) {
         // scalar path (rare): lane computes rows lane and lane+32 for every head
         const int b = u / L.heads, h = u - b * L.heads;
         const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
