@@ -32,8 +32,9 @@
 //  * V: rows are the MMA k dimension, the pack direction, so
 //    the decoded registers are the A fragment directly (no transpose).
 //    out = sum_t (w_t s_t) code + sum_t w_t z_t.
-// Blocks with a pack wider than 4 bits or a large minimum take a scalar path
-// inside the same launch (never at the default rel 0.1 / 0.2).
+// Blocks with packs of width 5..7 run a second, block-uniform unpack (four
+// 4-field spreads per pack); blocks with a width >= 8 or a large minimum take a
+// scalar path inside the same launch (never at the default rel 0.1 / 0.2).
 #include "pkv_common.cuh"
 
 #include <mutex>
@@ -160,7 +161,7 @@ __device__ __forceinline__ const uint8_t* gptr(const uint8_t* p) { return p; }
 __device__ __forceinline__ const uint8_t* gptr(uint32_t a) { return (const uint8_t*)__cvta_shared_to_generic(a); }
 
 // ---------------------------------------------------------------- unpack
-// Per-width constants (w <= 4): MA = 2^(16-4w), MB = 2^(32-2w), MC = 2^(8-w),
+// Per-width constants (w <= 8; MA only for w <= 4): MA = 2^(16-4w), MB = 2^(32-2w), MC = 2^(8-w),
 // byte mask (2^w - 1) * 0x01010101.  Entry w at lut + 16*w.
 __device__ __forceinline__ void init_lut(uint4* lut, int tid) {
   if (tid < 16) {
@@ -307,7 +308,7 @@ __device__ __forceinline__ uint32_t pack_min(const uint8_t* __restrict__ blk, in
 // Lane `chunk` reads the width nibbles of physical packs 16*chunk .. +15 and the
 // 16 minima of chunk `mchunk` (its own, or the chunk it will decode).  Returns the lane's starting payload bit (warp scan over chunks in
 // lane order) and whether every pack of the block fits the fast path
-// (w <= 4 and minimum <= 240, so min + 15 fits a byte).
+// (every code min + 2^w - 1 fits a byte, see below).
 struct Chunk {
   uint2 nb;       // 16 width nibbles
   uint32_t mn[8]; // 16 u16 minima
