@@ -365,7 +365,12 @@ def main():
     # PKV_BENCH_BACKEND=gloo (structural test of the N > 1 path with several ranks on
     # one device); production runs use NCCL, one rank per GPU
     backend = os.environ.get("PKV_BENCH_BACKEND", "nccl")
-    local = local % max(1, torch.cuda.device_count())
+    ndev = torch.cuda.device_count()
+    if backend == "nccl":
+        if local >= ndev:  # one NCCL rank per GPU: never two ranks on one device
+            raise SystemExit(f"LOCAL_RANK {local} >= {ndev} visible GPUs (NCCL needs one rank per GPU)")
+    else:
+        local = local % max(1, ndev)
     torch.cuda.set_device(local)
     if world > 1:
         if backend == "nccl":

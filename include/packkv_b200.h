@@ -48,6 +48,7 @@ enum {
 #define PKV_FLAG_WIDTH 2
 #define PKV_FLAG_MALFORMED 4
 #define PKV_FLAG_CAPACITY 8
+#define PKV_FLAG_SHAPE 16     /* score / weight row stride shorter than the token count */
 
 #define PKV_KIND_K 0
 #define PKV_KIND_V 1
@@ -92,6 +93,15 @@ typedef struct pkv_layer {
 
 const char* pkv_last_error(void);
 int pkv_version(void);
+/* Kernel family the calling thread's last fused call launched
+ * (pkv_fused_k_scores / pkv_fused_v_output / pkv_attention_decode):
+ * PKV_PATH_FAST = the default-format tensor-core kernels
+ * (fused_{k,v}_fast_kernel), PKV_PATH_GENERIC = the scalar kernels for every
+ * other format.  Lets tests assert which kernels they exercised.           */
+#define PKV_PATH_NONE 0
+#define PKV_PATH_FAST 1
+#define PKV_PATH_GENERIC 2
+int pkv_last_path(void);
 
 /* --- quantizer -------------------------------------- */
 /* quantize_token_wise over n independent [rows, cols] fp16 tensors.

@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 PKV_OK, PKV_E_SHAPE, PKV_E_NONFINITE, PKV_E_WIDTH, PKV_E_MALFORMED = 0, 1, 2, 3, 4
 PKV_E_INDEX, PKV_E_ARG, PKV_E_CUDA, PKV_E_CAPACITY = 5, 6, 7, 8
-FLAG_NONFINITE, FLAG_WIDTH, FLAG_MALFORMED, FLAG_CAPACITY = 1, 2, 4, 8
+FLAG_NONFINITE, FLAG_WIDTH, FLAG_MALFORMED, FLAG_CAPACITY, FLAG_SHAPE = 1, 2, 4, 8, 16
+PATH_NONE, PATH_FAST, PATH_GENERIC = 0, 1, 2
 REPACK = {"none": 0, "greedy": 1, "v_median": 2}
 REPACK_EXTERNAL = 3
 
@@ -45,6 +46,7 @@ class Layer(ctypes.Structure):
 _SIGS = {
     "pkv_last_error": (ctypes.c_char_p, []),
     "pkv_version": (c_int32, []),
+    "pkv_last_path": (c_int32, []),
     "pkv_quantize": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_float, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pkv_check_finite": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
     "pkv_dequantize": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
@@ -151,6 +153,13 @@ def raise_flags(flags: int, what: str = ""):
         raise E.MalformedBlockError(f"{what}: block header or length invalid")
     if flags & FLAG_CAPACITY:
         raise CapacityError(f"{what}: arena capacity exceeded")
+    if flags & FLAG_SHAPE:
+        raise E.ShapeMismatchError(f"{what}: score / weight row stride shorter than the token count")
+
+
+def last_path() -> int:
+    """PATH_FAST / PATH_GENERIC: kernel family of this thread's last fused call."""
+    return int(load().pkv_last_path())
 
 
 def ptr(t) -> int:

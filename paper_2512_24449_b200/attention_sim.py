@@ -58,6 +58,10 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     return fused_v_output_batched(store, layer, a, out=out)
 
 
+def ptr_of(t):
+    return 0 if t is None else t.data_ptr()
+
+
 class _Captured:
     """Shared machinery: static input/output buffers allocated OUTSIDE the
     capture (so capturing allocates nothing), a capture key over the state the
@@ -73,8 +77,11 @@ class _Captured:
 
     def _state(self, q: torch.Tensor):
         ls = self.store[self.layer]
+        # every device buffer the recorded launches read or write: a re-allocated
+        # scratch / score / output buffer must force a re-capture, not a replay
+        # against freed memory
         return (ls.nblk_h, ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(), tuple(q.shape),
-                q.device)
+                q.device, ls.a_scratch.data_ptr(), ptr_of(self._scores), ptr_of(self._out))
 
     def _buffers(self, q: torch.Tensor):
         st = self.store
@@ -148,7 +155,7 @@ class GraphedAttention(_Captured):
             self._buffers(q)
             self._attend(self._q)  # warm-up outside capture (scratch, occupancy queries)
             self._capture(lambda: self._attend(self._q))
-            self._key = key
+            self._key = self._state(q)  # after _buffers: the captured buffers' addresses
         self._q.copy_(q, non_blocking=True)
         self._graph.replay()
         return self._out
@@ -192,7 +199,7 @@ class GraphedDecodeStep(_Captured):
                                                 N.stream()), "stage_token")
                 self._attend(self._q)
             self._capture(record)
-            self._key = key
+            self._key = self._state(q)  # after _buffers: the captured buffers' addresses
         for dst, src in ((self._k, k), (self._v, v), (self._q, q)):
             if dst.data_ptr() != src.data_ptr():  # callers may write the inputs() in place
                 dst.copy_(src, non_blocking=True)

@@ -5,6 +5,9 @@
 #include "pkv_common.cuh"
 
 static thread_local char g_last_error[512] = "";
+static thread_local int g_last_path = PKV_PATH_NONE;
+
+void pkv_note_path(int path) { g_last_path = path; }
 
 void pkv_set_error(const char* fmt, ...) {
   va_list ap;
@@ -22,3 +25,5 @@ int pkv_cuda_status(cudaError_t e, const char* what) {
 extern "C" const char* pkv_last_error(void) { return g_last_error; }
 
 extern "C" int pkv_version(void) { return PKV_ABI_VERSION; }
+
+extern "C" int pkv_last_path(void) { return g_last_path; }

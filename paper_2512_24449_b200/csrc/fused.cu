@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kNW * 32) fused_k_kernel(pkv_layer_t L, const 
     __syncwarp();
   }
   if (blockIdx.x == 0) {  // uncompressed residue (staged tokens), same launch
-    const int nr = L.nres[b];
+    const int nr = res_rows(L, b, sstride);
     const uint16_t* kr = L.stage + (int64_t(0) * U + u) * L.buffer * D;
     for (int t = warp; t < nr; t += kNW) {
       for (int gq = 0; gq < G; ++gq) {
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kNW * 32) fused_v_kernel(pkv_layer_t L, const 
     __syncwarp();
   }
   if (blockIdx.x == 0) {  // residue, same launch; warps split tokens
-    const int nr = L.nres[b];
+    const int nr = res_rows(L, b, wstride);
     const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * D;
     for (int t = warp; t < nr; t += kNW) {
 #pragma unroll
@@ -367,13 +367,17 @@ extern "C" int pkv_fused_k_scores(const pkv_layer_t* L, int32_t nblocks, const f
   int G = 0;
   int s = fused_args(L, nblocks, q_heads, &G);
   if (s) return s;
-  if (score_stride < int64_t(nblocks) * 64 + L->buffer && score_stride < int64_t(nblocks) * 64) {
-    pkv_set_error("score_stride too small");
+  if (score_stride < int64_t(nblocks) * L->block) {
+    pkv_set_error("score_stride %lld < nblocks * block = %lld", (long long)score_stride,
+                  (long long)nblocks * L->block);
     return PKV_E_SHAPE;
   }
   cudaStream_t strm = (cudaStream_t)stream;
-  if (pkv_fast_supported(L, G, score_stride) && (reinterpret_cast<uintptr_t>(q) & 15) == 0)
+  if (pkv_fast_supported(L, G, score_stride) && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+    pkv_note_path(PKV_PATH_FAST);
     return pkv_fast_fused_k(L, nblocks, q, G, scores, score_stride, strm);
+  }
+  pkv_note_path(PKV_PATH_GENERIC);
   PKV_DISPATCH_KD(L->pack_size, L->head_dim, return (launch_k<KPc, Dc>(L, nblocks, q, G, scores, score_stride, strm)));
   return PKV_OK;
 }
@@ -397,10 +401,17 @@ extern "C" int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const f
     pkv_set_error("V scratch too small");
     return PKV_E_ARG;
   }
+  if (w_stride < int64_t(nblocks) * L->block) {
+    pkv_set_error("w_stride %lld < nblocks * block = %lld", (long long)w_stride, (long long)nblocks * L->block);
+    return PKV_E_SHAPE;
+  }
   cudaStream_t strm = (cudaStream_t)stream;
   float* part = (float*)scratch;
-  if (pkv_fast_supported(L, G, w_stride) && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
+  if (pkv_fast_supported(L, G, w_stride)) {
+    pkv_note_path(PKV_PATH_FAST);
     return pkv_fast_fused_v(L, nblocks, w, G, w_stride, out, part, strm);
+  }
+  pkv_note_path(PKV_PATH_GENERIC);
   if (G <= 4) {
     PKV_DISPATCH_KD(L->pack_size, L->head_dim,
                     return (launch_v<KPc, Dc, 4>(L, nblocks, w, G, w_stride, out, part, strm)));
@@ -424,18 +435,19 @@ extern "C" int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const
   int G = 0;
   int s = fused_args(L, nblocks, q_heads, &G);
   if (s) return s;
-  if (!pkv_fast_supported(L, G, score_stride) || (reinterpret_cast<uintptr_t>(q) & 15) ||
-      (reinterpret_cast<uintptr_t>(scores) & 15)) {
+  if (!pkv_fast_supported(L, G, score_stride) || (reinterpret_cast<uintptr_t>(q) & 15)) {
     pkv_set_error("attention_decode: only the default format (pack 16, head_dim 128, block 64, G <= 8) is fused");
     return PKV_E_ARG;
   }
-  if (score_stride < int64_t(nblocks) * 64 + L->buffer && score_stride < int64_t(nblocks) * 64) {
-    pkv_set_error("score_stride too small");
+  if (score_stride < int64_t(nblocks) * L->block) {
+    pkv_set_error("score_stride %lld < nblocks * block = %lld", (long long)score_stride,
+                  (long long)nblocks * L->block);
     return PKV_E_SHAPE;
   }
   if (scratch_bytes < pkv_fast_attention_scratch(L, nblocks, G)) {
     pkv_set_error("attention scratch too small");
     return PKV_E_ARG;
   }
+  pkv_note_path(PKV_PATH_FAST);
   return pkv_fast_attention(L, nblocks, q, G, scores, score_stride, out, (float*)scratch, (cudaStream_t)stream);
 }

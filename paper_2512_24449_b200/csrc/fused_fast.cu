@@ -928,7 +928,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   for (int64_t uu = wid; uu < U; uu += nwarps) {
     const int u = int(uu);
     const int b = u / L.heads, h = u - b * L.heads;
-    const int nr = L.nres[b];
+    const int nr = res_rows(L, b, sstride);
     float rm[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) rm[g] = -INFINITY;
@@ -1101,7 +1101,9 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
     ++seg;
   };
 
-  // weights of the next block (prefetched one block ahead)
+  // weights of the next block (prefetched one block ahead); vector loads when
+  // every row starts 16-byte aligned, else scalar (any w_stride)
+  const bool wvec = (wstride & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
   float wn[TPL];
   auto load_w = [&](int k, const Cursor& c) {
     const int b = c.u / L.heads, h = c.u - b * L.heads;
@@ -1110,7 +1112,13 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
 #pragma unroll
     for (int q4 = 0; q4 < TPL / 4; ++q4) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ok) v = *(const float4*)(wrow + 4 * q4);
+      if (ok) {
+        if (wvec) {
+          v = *(const float4*)(wrow + 4 * q4);
+        } else {  // any row stride (rows not 16-byte aligned): scalar loads
+          v.x = wrow[4 * q4]; v.y = wrow[4 * q4 + 1]; v.z = wrow[4 * q4 + 2]; v.w = wrow[4 * q4 + 3];
+        }
+      }
       wn[4 * q4] = v.x; wn[4 * q4 + 1] = v.y; wn[4 * q4 + 2] = v.z; wn[4 * q4 + 3] = v.w;
     }
   };
@@ -1146,11 +1154,17 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
     auto process = [&](auto blk, bool may_fast) {
       Chunk ch;
       const int src = 8 * tq + gi;  // the chunk this lane decodes (row-group tq, channels 16gi..)
-      const bool fast = parse_chunk(blk, lane, src, ch) && may_fast;
-      // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits, f a power of two
-      // per (block, head) with max x * f < 2^16; z term sum_t w_t z_t in f32
+      const bool fast0 = parse_chunk(blk, lane, src, ch) && may_fast;
+      // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits scaled per
+      // (block, head) by f = 65535 / max x, so every x is rounded to nearest at
+      // 2^-16 of the block's largest (the digit sums are exact in int32); z term
+      // sum_t w_t z_t in f32.  A block with a negative x (w is any real vector,
+      // SPEC.md:455-463; softmax weights never are) takes the scalar f32 path:
+      // signed digits would lose the precision the code / zero-point cancellation
+      // needs (out = sum x*code + sum w*z nearly cancels on centred V).
       float xs[TPL];
       float mx = 0.f;
+      bool neg = false;
       if (SM) {
 #pragma unroll
         for (int e = 0; e < TPL; ++e) {
@@ -1166,14 +1180,13 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
         xs[2 * e2] = wc[2 * e2] * s0;
         xs[2 * e2 + 1] = wc[2 * e2 + 1] * s1;
         mx = fmaxf(mx, fmaxf(xs[2 * e2], xs[2 * e2 + 1]));
+        neg |= (xs[2 * e2] < 0.f) | (xs[2 * e2 + 1] < 0.f);
       }
+      const bool fast = fast0 && !__any_sync(PKV_FULL, neg);
 #pragma unroll
       for (int o = 1; o < LPH; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(PKV_FULL, mx, o));
-      // f = 2^(15 - e) for mx in [2^e, 2^(e+1)): mx * f < 2^16
-      const int eb = (__float_as_int(mx) >> 23) & 0xff;
-      const int fb = min(269 - eb, 254);
-      const float f = __int_as_float(fb << 23);
-      const float invf = __int_as_float((254 - fb) << 23);
+      const float f = mx > 1e-30f ? __fdiv_rn(65535.f, mx) : 0.f;
+      const float invf = mx > 1e-30f ? __fdiv_rn(mx, 65535.f) : 0.f;
 #pragma unroll
       for (int e8 = 0; e8 < TPL / 8; ++e8) {
         uint32_t v[8];
@@ -1181,7 +1194,6 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
         // round to nearest (unbiased: a softmax-weighted block sums many small
         // x·f with errors of both signs), clamped so 65535.5+ cannot carry
         for (int e = 0; e < 8; ++e) v[e] = min(__float_as_uint(__fmaf_rn(xs[8 * e8 + e], f, 8388608.f)), 0x4B00FFFFu);
-        // byte position p holds row tok(p): (0,1,4,5) then (2,3,6,7)
         const uint32_t t01 = __byte_perm(v[0], v[1], 0x5140), t45 = __byte_perm(v[4], v[5], 0x5140);
         const uint32_t t23 = __byte_perm(v[2], v[3], 0x5140), t67 = __byte_perm(v[6], v[7], 0x5140);
         const uint32_t lo0 = __byte_perm(t01, t45, 0x5410), hi0 = __byte_perm(t01, t45, 0x7632);
@@ -1364,7 +1376,7 @@ __global__ void __launch_bounds__(512) fused_v_fast_finalize(pkv_layer_t L, cons
     // residue rows (< 64): row t goes to thread group t % 4, 8 loads in flight
     {
       const int b = u / L.heads;
-      const int nr = L.nres[b];
+      const int nr = res_rows(L, b, wstride);
       const float* wr = w + (int64_t(b) * L.heads * G + int64_t(u - b * L.heads) * G + g) * wstride + int64_t(L.nblk[b]) * kRows;
       const uint16_t* vr = L.stage + (int64_t(1) * U + u) * L.buffer * kD;
       if (SM) __syncthreads();  // Msh
@@ -1505,8 +1517,11 @@ void launch_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t 
 
 }  // namespace
 
+// Any score / weight row stride: K writes scores with scalar stores, V picks
+// vector or scalar weight loads per launch (wvec).
 bool pkv_fast_supported(const pkv_layer_t* L, int G, int64_t stride) {
-  return L->pack_size == kP && L->head_dim == kD && L->block == kRows && G >= 1 && G <= 8 && stride % 4 == 0;
+  (void)stride;
+  return L->pack_size == kP && L->head_dim == kD && L->block == kRows && G >= 1 && G <= 8;
 }
 
 int pkv_fast_fused_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,

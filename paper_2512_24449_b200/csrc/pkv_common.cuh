@@ -135,8 +135,21 @@ __device__ __forceinline__ void set_flag(int32_t* err, int32_t bit) {
   if (err) atomicOr(err, bit);
 }
 
+// Residue rows of sequence b that fit a score / weight row of `stride` floats
+// (rows nblk*block + t, t < nres).  A caller stride shorter than the token
+// count drops the rows past it and raises PKV_FLAG_SHAPE (ShapeMismatchError)
+// instead of writing / reading into the next head's row.
+__device__ __forceinline__ int res_rows(const pkv_layer_t& L, int b, int64_t stride) {
+  const int nr = L.nres[b];
+  const int64_t room = stride - int64_t(L.nblk[b]) * L.block;
+  if (int64_t(nr) <= room) return nr;
+  if (threadIdx.x % 32 == 0) set_flag(L.err, PKV_FLAG_SHAPE);
+  return room > 0 ? int(room) : 0;
+}
+
 }  // namespace pkv
 
 // host-side helpers (defined in capi.cu)
 void pkv_set_error(const char* fmt, ...);
 int pkv_cuda_status(cudaError_t e, const char* what);
+void pkv_note_path(int path);  // records the kernel family for pkv_last_path()

@@ -509,6 +509,22 @@ def load_store(path, device=None, check: bool = True) -> CompressedStore:
         offs, lens = rec["off"].astype(np.int64), rec["len"].astype(np.int64)
         if ((offs % 16) != 0).any() or (offs + lens > alen).any() or (lens < hb).any():
             raise E.StoreFormatError(f"{path}: bad directory record")
+        if len(offs):
+            # records may not overlap (the arena is append-only)
+            order = np.argsort(offs, kind="stable")
+            if (offs[order][:-1] + lens[order][:-1] > offs[order][1:]).any():
+                raise E.StoreFormatError(f"{path}: overlapping directory records")
+            # every record's length must equal its header plus the payload bytes its
+            # width nibbles promise (the fused kernels locate payloads from the
+            # nibbles alone, MalformedBlockError in decode_block)
+            P = (block // k) * head_dim
+            nib = arena[offs[:, None] + 8 + np.arange((P + 1) // 2)[None, :]]
+            wid = np.stack([nib & 15, nib >> 4], axis=-1).reshape(len(offs), -1)[:, :P].astype(np.int64)
+            expect = hb + ((k * wid + 7) // 8).sum(axis=1)
+            if (expect != lens).any():
+                i = int(np.nonzero(expect != lens)[0][0])
+                raise E.StoreFormatError(f"{path}: block {i} length {int(lens[i])} disagrees with its widths "
+                                         f"({int(expect[i])} bytes)")
         for i in range(len(offs)):                  # header geometry of every block
             o0 = int(offs[i])
             kind = (i // heads) % 2

@@ -79,3 +79,44 @@ def test_native_error_mapping():
         N.raise_flags(N.FLAG_NONFINITE | N.FLAG_WIDTH)
     with pytest.raises(IndexError):
         N.check(N.PKV_E_INDEX)
+
+
+def test_packkv_alias_resolves_to_the_implementation():
+    import packkv
+    import packkv.errors
+    import packkv.fused_kernels
+    import paper_2512_24449_b200.errors as E
+    import paper_2512_24449_b200.fused_kernels as F
+    assert packkv.errors is E and packkv.fused_kernels is F
+    assert hasattr(packkv.kv_store, "CompressedStore") and hasattr(packkv.fused_kernels, "fused_k_scores")
+
+
+def test_errors_subclass_the_installed_reference_classes(tmp_path):
+    """With the reference package importable as `packkv` (baseline/_ref, the
+    offline install of /root/reference/pkg), every error class of this
+    implementation is also the reference class of the same name, so existing
+    `except packkv.errors.X` handlers catch it (errors.py:4-41)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.exists(os.path.join(ref, "packkv", "errors.py")):
+        pytest.skip("reference package not installed in baseline/_ref")
+    import subprocess
+    import sys
+    pk = tmp_path / "pk"
+    pk.mkdir()
+    (pk / "paper_2512_24449_b200").symlink_to(os.path.join(ROOT, "paper_2512_24449_b200"))
+    code = ("import packkv.errors as R\n"
+            "from paper_2512_24449_b200 import errors as E\n"
+            "assert R.__file__.startswith(%r)\n"
+            "names = ['PackKVError', 'DumpFormatError', 'BadMagicError', 'TruncatedDumpError', 'NonFiniteValueError',\n"
+            "         'ShapeMismatchError', 'WidthOverflowError', 'MalformedBlockError', 'InstanceTooLargeError',\n"
+            "         'StoreFormatError']\n"
+            "for n in names:\n"
+            "    assert issubclass(getattr(E, n), getattr(R, n)), n\n"
+            "try:\n"
+            "    raise E.BadMagicError('x')\n"
+            "except R.DumpFormatError:\n"
+            "    pass\n"
+            "print('ok')\n") % ref
+    env = dict(os.environ, PYTHONPATH=f"{ref}{os.pathsep}{pk}")
+    r = subprocess.run([sys.executable, "-c", code], cwd=str(tmp_path), env=env, capture_output=True, text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr
