@@ -315,8 +315,12 @@ struct Chunk {
   uint32_t bit;   // payload bit offset of the chunk's first pack
   bool wide;      // the block has a pack of width 5..8 (warp-uniform)
 };
+// The parse in three steps so a caller can overlap it with independent work
+// (the V kernel's weight operand): loads, per-lane statistics, then one warp
+// vote (flag bits below, OR-reduced) and the 5-step scan.
+enum : uint32_t { kFWide = 1, kFGe8 = 2, kFMin240 = 4, kFMin128 = 8, kFNeg = 16 };
 template <class P>
-__device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& ch) {
+__device__ __forceinline__ void parse_load(P blk, int lane, int mchunk, Chunk& ch) {
   ch.nb = ld64(blk + kNib + 8 * lane);
   // minima of chunk `mchunk` (32 bytes at kMin + 32*mchunk = 264 + 32*mchunk):
   // three aligned 16-byte loads from 256 + 32*mchunk, words 2..9
@@ -324,18 +328,29 @@ __device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& 
               m2 = ld128(blk + kMin + 24 + 32 * mchunk);
   ch.mn[0] = m0.z; ch.mn[1] = m0.w; ch.mn[2] = m1.x; ch.mn[3] = m1.y;
   ch.mn[4] = m1.z; ch.mn[5] = m1.w; ch.mn[6] = m2.x; ch.mn[7] = m2.y;
+}
+// this lane's flag bits: a pack of width 5..8 (kFWide), of width >= 8 (kFGe8),
+// a minimum above 240 / 128.  The fast path needs every code min + 2^w - 1 to
+// fit a byte: w <= 4 everywhere and minima <= 240, or w <= 7 and minima <= 128
+// (w = 8 packs and larger minima take the scalar path).
+__device__ __forceinline__ uint32_t parse_flags(const Chunk& ch) {
   uint32_t mor = 0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) mor |= ch.mn[q];
   const uint32_t nx = ch.nb.x, ny = ch.nb.y;
-  // w <= 4 everywhere and minima <= 240, or w <= 7 and minima <= 128: every
-  // code min + 2^w - 1 fits a byte (w = 8 packs and larger minima: scalar path)
   const uint32_t ge8 = (nx | ny) & 0x88888888u;
   const uint32_t ge5 = (((nx >> 2) & (nx | (nx >> 1))) & 0x11111111u) | (((ny >> 2) & (ny | (ny >> 1))) & 0x11111111u);
-  // (warp-wide: in V a lane checks the widths of one chunk and the minima of another)
   const uint32_t mo = (mor | (mor >> 16)) & 0xffffu;
-  ch.wide = __any_sync(PKV_FULL, ge5 != 0u);
-  const bool ok = ge8 == 0 && mo <= (ch.wide ? 128u : 240u);
+  return (ge5 ? kFWide : 0u) | (ge8 ? kFGe8 : 0u) | (mo > 240u ? kFMin240 : 0u) | (mo > 128u ? kFMin128 : 0u);
+}
+// warp-OR of the flags -> fast-path verdict and ch.wide
+__device__ __forceinline__ bool parse_verdict(uint32_t all, Chunk& ch) {
+  ch.wide = (all & kFWide) != 0;
+  return !(all & (kFGe8 | kFNeg | (ch.wide ? kFMin128 : kFMin240)));
+}
+// ch.bit = payload bit offset of chunk `lane` (warp scan over chunks in lane order)
+__device__ __forceinline__ void parse_scan(int lane, Chunk& ch) {
+  const uint32_t nx = ch.nb.x, ny = ch.nb.y;
   uint32_t a = (nx & 0x0f0f0f0fu) + ((nx >> 4) & 0x0f0f0f0fu) + (ny & 0x0f0f0f0fu) + ((ny >> 4) & 0x0f0f0f0fu);
   a = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu);
   const uint32_t lsum = 16u * ((a & 0xffffu) + (a >> 16));  // payload bits (k = 16)
@@ -346,7 +361,17 @@ __device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& 
     if (lane >= o) inc += y;
   }
   ch.bit = 8u * kHdr + inc - lsum;
-  return __all_sync(PKV_FULL, ok);
+}
+// Lane `chunk` reads the width nibbles of physical packs 16*chunk .. +15 and the
+// 16 minima of chunk `mchunk` (its own, or the chunk it will decode).  Returns
+// whether every pack of the block fits the fast path; ch.bit is the lane's
+// starting payload bit.
+template <class P>
+__device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& ch) {
+  parse_load(blk, lane, mchunk, ch);
+  const bool fast = parse_verdict(__reduce_or_sync(PKV_FULL, parse_flags(ch)), ch);
+  parse_scan(lane, ch);
+  return fast;
 }
 
 // Slow-path descriptor table for any widths: desc[p] = payload bit (from the
@@ -392,18 +417,25 @@ __host__ __device__ __forceinline__ int64_t warp_of(int64_t gb, int64_t total, i
   return nwarps > total ? gb : ((gb + 1) * nwarps - 1) / total;
 }
 
-// Position (unit u, block j) of a global block index, advanced without division.
+// Position (unit u = b * heads + h, block j) of a global block index,
+// advanced without division.
 struct Cursor {
-  int u, j;
-  __device__ __forceinline__ void init(int64_t gb, int NB) {
+  int u, j, b, h;
+  __device__ __forceinline__ void init(int64_t gb, int NB, int heads) {
     u = int(gb / NB);
     j = int(gb - int64_t(u) * NB);
+    b = u / heads;
+    h = u - b * heads;
   }
-  __device__ __forceinline__ void step(int by, int NB) {
+  __device__ __forceinline__ void step(int by, int NB, int heads) {
     j += by;
     while (j >= NB) {
       j -= NB;
       ++u;
+      if (++h == heads) {
+        h = 0;
+        ++b;
+      }
     }
   }
 };
@@ -429,6 +461,7 @@ struct Feed {
   uint32_t* pos;     // [NS] ring offset of the block in the slot
   uint32_t* abs;     // [NS] absolute start (for space accounting)
   const uint8_t** gsrc;  // [NS] non-null: block larger than the ring, read in place from global memory
+  int* present;      // [NS] 1: the slot holds a block (0: past the sequence's nblk)
   uint32_t head;     // absolute allocation point
   int issued;        // blocks issued so far
   // directory of the warp's blocks, lane-distributed: entry k0 + lane
@@ -442,6 +475,7 @@ struct Feed {
     gsrc = (const uint8_t**)(bar + NS);
     pos = (uint32_t*)(gsrc + NS);
     abs = pos + NS;
+    present = (int*)(abs + NS);
     head = 0;
     issued = 0;
     k0 = -32;
@@ -451,7 +485,7 @@ struct Feed {
     }
     __syncwarp();
   }
-  static constexpr size_t bytes() { return RB + NS * 24; }
+  static constexpr size_t bytes() { return RB + NS * 28; }
 
   // (re)load the directory entries of the warp's blocks kk .. kk+31
   __device__ __forceinline__ void load_dir(const pkv_layer_t& L, int kind, int NB, const Range& rg, int kk, int lane) {
@@ -492,6 +526,7 @@ struct Feed {
       pos[s] = p;
       abs[s] = head + skip;
       gsrc[s] = big ? L.arena + off : nullptr;
+      present[s] = len >= 0;
       if (len < 0 || big) {
         mbar_arrive(&bar[s]);
       } else {
@@ -528,10 +563,16 @@ struct Feed {
   // wait for block k; returns its bytes in the ring, or sets *g to the block
   // in global memory when it was too large to stage (then the ring pointer is
   // meaningless)
-  __device__ __forceinline__ uint32_t wait(int k, const uint8_t** g) {
+  // (*have = the block exists: a sequence shorter than the grid's block count
+  // has no block there.  Read from shared memory, so the test never waits on a
+  // global-load scoreboard shared with loads just issued, e.g. the next
+  // block's weights: ~16% of the V kernel's time stalled there with nblk[b]
+  // read from global memory.)
+  __device__ __forceinline__ uint32_t wait(int k, const uint8_t** g, bool* have) {
     const int s = k % NS;
     mbar_wait(&bar[s], uint32_t((k / NS) & 1));
     *g = gsrc[s];
+    *have = present[s] != 0;
     return smem_u32(ring) + pos[s];
   }
 };
@@ -695,7 +736,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   const Range rg = warp_range(total, wid, nwarps);
   const int nk = int(rg.b1 - rg.b0);
   QFrag<NU> Q;
-  int cur_u = -1, nbk = 0;
+  int cur_u = -1;
   float* sbase = scores;
   float kmx0 = -INFINITY, kmx1 = -INFINITY;  // running max of this lane's scores (heads tq, tq + 4)
   // the unit's score maxima of this warp -> kmax[u][slot][g] (lanes with gi = 0 write)
@@ -712,7 +753,7 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
     kmx0 = kmx1 = -INFINITY;
   };
   Cursor cs;
-  cs.init(rg.b0, NB);
+  cs.init(rg.b0, NB, L.heads);
 #if PKV_DIAG_WAITCLK
   long long dwait = 0;
   const long long tstart = clock64();
@@ -720,13 +761,12 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   F.refill(L, 0, NB, rg, nk, -1, 0u, lane);
 
 #pragma unroll 1
-  for (int k = 0; k < nk; ++k, cs.step(1, NB)) {
+  for (int k = 0; k < nk; ++k, cs.step(1, NB, L.heads)) {
     const int u = cs.u, j = cs.j;
     if (u != cur_u) {
       if (ST && cur_u >= 0) flush_max(cur_u);
       cur_u = u;
-      const int b = u / L.heads, h = u - b * L.heads;
-      nbk = L.nblk[b];
+      const int b = cs.b, h = cs.h;
       sbase = scores + (int64_t(b) * Hq + int64_t(h) * G) * sstride;
       build_qfrag<NU>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, Q);
     }
@@ -734,22 +774,23 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
 #if PKV_DIAG_WAITCLK
     const long long tw0 = clock64();
 #endif
-    const uint32_t blk = F.wait(k, &gblk);
+    bool have;
+    const uint32_t blk = F.wait(k, &gblk, &have);
 #if PKV_DIAG_WAITCLK
     dwait += clock64() - tw0;
 #endif
 #if PKV_DIAG_FEEDONLY
-    if (j < nbk && lane == 0) sbase[j] = __uint_as_float(ld32(blk));
+    if (have && lane == 0) sbase[j] = __uint_as_float(ld32(blk));
     if (false) {
 #elif PKV_DIAG_FEEDPARSE
-    if (j < nbk) {
+    if (have) {
       Chunk ch;
       const bool fast = gblk == nullptr && parse_chunk(blk, lane, lane, ch);
       if (lane == 0) sbase[j] = __uint_as_float(ch.bit + fast + ch.mn[3] + ch.nb.y);
     }
     if (false) {
 #else
-    if (j < nbk) {
+    if (have) {
 #endif
       Chunk ch;
       // the fast path on the staged copy, or in place (global loads) on a block
@@ -1003,6 +1044,9 @@ __device__ __forceinline__ float row_max(const float* __restrict__ kmax, const f
   return m;
 }
 constexpr int kWV = 4;
+#ifndef PKV_VPIPE  // V: load the next pack pair while decoding the current one
+#define PKV_VPIPE 1
+#endif
 #ifndef PKV_VMINB  // V: CTAs per SM the register allocation must allow
 #define PKV_VMINB 4
 #endif
@@ -1106,8 +1150,7 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
   const bool wvec = (wstride & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
   float wn[TPL];
   auto load_w = [&](int k, const Cursor& c) {
-    const int b = c.u / L.heads, h = c.u - b * L.heads;
-    const float* wrow = w + (int64_t(b) * Hq + int64_t(h) * G + wh) * wstride + int64_t(c.j) * kRows + wt0;
+    const float* wrow = w + (int64_t(c.b) * Hq + int64_t(c.h) * G + wh) * wstride + int64_t(c.j) * kRows + wt0;
     const bool ok = k < nk && wh < G;
 #pragma unroll
     for (int q4 = 0; q4 < TPL / 4; ++q4) {
@@ -1123,10 +1166,14 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
     }
   };
   Cursor cs, cn;
-  cs.init(rg.b0, NB);
+  cs.init(rg.b0, NB, L.heads);
   cn = cs;
   load_w(0, cn);
-  int cur_u = -1, b = 0, h = 0, nbk = 0;
+  int cur_u = -1, b = 0, h = 0;
+#if PKV_DIAG_WAITCLK
+  long long dwait = 0;
+  const long long tstart = clock64();
+#endif
   F.refill(L, 1, NB, rg, nk, -1, 0u, lane);
 
 #pragma unroll 1
@@ -1134,27 +1181,32 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
     const int u = cs.u, j = cs.j;
     if (u != cur_u) {
       cur_u = u;
-      b = u / L.heads;
-      h = u - b * L.heads;
-      nbk = L.nblk[b];
+      b = cs.b;
+      h = cs.h;
       if (SM) Mh = row_max(kmax, kres, u, wh < G ? wh : 0, G, NB, ktotal, knwarps, kslots, lane % LPH, LPH) * 1.4426950408889634f;
     }
     while (seg < u - u_first) flush();
     float wc[TPL];
 #pragma unroll
     for (int e = 0; e < TPL; ++e) wc[e] = wn[e];
-    cn.step(1, NB);
+    cn.step(1, NB, L.heads);
     load_w(k + 1, cn);
     cs = cn;
     const uint8_t* gblk;
-    const uint32_t sblk = F.wait(k, &gblk);
+#if PKV_DIAG_WAITCLK
+    const long long tw0 = clock64();
+#endif
+    bool have;
+    const uint32_t sblk = F.wait(k, &gblk, &have);
+#if PKV_DIAG_WAITCLK
+    dwait += clock64() - tw0;
+#endif
     // one block: B operand, then the IMMA fast path or the scalar path.  Called
     // with the shared-memory copy (LDS), or for a block too large to stage with
     // the global-memory block (generic loads, scalar path only).
     auto process = [&](auto blk, bool may_fast) {
       Chunk ch;
       const int src = 8 * tq + gi;  // the chunk this lane decodes (row-group tq, channels 16gi..)
-      const bool fast0 = parse_chunk(blk, lane, src, ch) && may_fast;
       // ---- B operand: x_t = w_t * s_t as 2 unsigned byte digits scaled per
       // (block, head) by f = 65535 / max x, so every x is rounded to nearest at
       // 2^-16 of the block's largest (the digit sums are exact in int32); z term
@@ -1162,6 +1214,13 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
       // SPEC.md:455-463; softmax weights never are) takes the scalar f32 path:
       // signed digits would lose the precision the code / zero-point cancellation
       // needs (out = sum x*code + sum w*z nearly cancels on centred V).
+      // The parse (loads, flags, scan) and the operand (params, x, max) are
+      // independent chains: loads first, one vote, the two shuffle chains
+      // interleaved.
+      parse_load(blk, lane, src, ch);
+      uint2 pr[TPL / 2];
+#pragma unroll
+      for (int e2 = 0; e2 < TPL / 2; ++e2) pr[e2] = ld64(blk + kPar + 4 * (wt0 + 2 * e2));
       float xs[TPL];
       float mx = 0.f;
       bool neg = false;
@@ -1174,19 +1233,21 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
       }
 #pragma unroll
       for (int e2 = 0; e2 < TPL / 2; ++e2) {
-        const uint2 pr = ld64(blk + kPar + 4 * (wt0 + 2 * e2));
-        const float s0 = h2f(pr.x & 0xffff), s1 = h2f(pr.y & 0xffff);
-        zacc = fmaf(wc[2 * e2], h2f(pr.x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr.y >> 16), zacc));
+        const float s0 = h2f(pr[e2].x & 0xffff), s1 = h2f(pr[e2].y & 0xffff);
+        zacc = fmaf(wc[2 * e2], h2f(pr[e2].x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr[e2].y >> 16), zacc));
         xs[2 * e2] = wc[2 * e2] * s0;
         xs[2 * e2 + 1] = wc[2 * e2 + 1] * s1;
         mx = fmaxf(mx, fmaxf(xs[2 * e2], xs[2 * e2 + 1]));
         neg |= (xs[2 * e2] < 0.f) | (xs[2 * e2 + 1] < 0.f);
       }
-      const bool fast = fast0 && !__any_sync(PKV_FULL, neg);
+      const uint32_t flags = parse_flags(ch) | (neg ? uint32_t(kFNeg) : 0u);
+      const bool fast = parse_verdict(__reduce_or_sync(PKV_FULL, flags), ch) && may_fast;
+      parse_scan(lane, ch);
 #pragma unroll
       for (int o = 1; o < LPH; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(PKV_FULL, mx, o));
-      const float f = mx > 1e-30f ? __fdiv_rn(65535.f, mx) : 0.f;
-      const float invf = mx > 1e-30f ? __fdiv_rn(mx, 65535.f) : 0.f;
+      // (f only needs f * invf ~ 1 and max x * f <= 65535.5, the clamp below)
+      const float f = mx > 1e-30f ? __fdividef(65535.f, mx) : 0.f;
+      const float invf = mx * (1.f / 65535.f);
 #pragma unroll
       for (int e8 = 0; e8 < TPL / 8; ++e8) {
         uint32_t v[8];
@@ -1218,11 +1279,23 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
         const uint32_t (&mn)[8] = ch.mn;
         // the m-tile's two packs decoded together, the next pair's loads in flight
         auto decode_mma = [&](auto wide) {
+#if PKV_VPIPE
           uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
           PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
+#endif
   #pragma unroll
           for (int mt = 0; mt < 8; ++mt) {
             uint32_t P[2][4];
+#if !PKV_VPIPE
+            {  // no cross-pair load pipelining: fewer live registers, latency hidden by more warps
+              const int i2 = 2 * mt;
+              const uint32_t wa = w16_of(nb, i2), wb = w16_of(nb, i2 + 1);
+              const PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
+              pack_decode<decltype(wide)::value>(blk, A, bit, wa, min_rep(mn, i2), P[0]);
+              pack_decode<decltype(wide)::value>(blk, B, bit + wa, wb, min_rep(mn, i2 + 1), P[1]);
+              bit += wa + wb;
+            }
+#else
             {
               const int i2 = 2 * mt;
               const uint32_t bitA = bit, bitB = bit + wa;
@@ -1245,6 +1318,7 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
                 B = nB;
               }
             }
+#endif
   #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
               int d[4] = {0, 0, 0, 0};
@@ -1306,7 +1380,7 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
       }
       __syncwarp();
     };
-    if (j < nbk) {
+    if (have) {
       if (gblk)
         process(gblk, false);
       else
@@ -1314,6 +1388,16 @@ __global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_l
     }
     F.refill(L, 1, NB, rg, nk, k, F.tail_after(k), lane);
   }
+#if PKV_DIAG_WAITCLK
+  __syncwarp();
+  if (lane == 0) {  // (wait cycles, loop cycles, blocks) per warp at the start of the partials
+    long long* dbg = reinterpret_cast<long long*>(part) + 3 * wid;
+    dbg[0] = dwait;
+    dbg[1] = clock64() - tstart;
+    dbg[2] = nk;
+  }
+  return;
+#endif
   while (seg <= u_last - u_first) flush();
 }
 
