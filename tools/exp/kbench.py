@@ -37,14 +37,14 @@ for name in a.which:
         g.capture_begin(); fn(); g.capture_end()
     torch.cuda.synchronize()
     ts = []
-    for _ in range(a.reps):  # 4 back-to-back replays per event pair (timer granularity ~2 us)
+    for _ in range(a.reps):  # 16 back-to-back replays per event pair (timer granularity ~2 us)
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(4):
+        for _ in range(16):
             g.replay()
         e1.record(); torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e3 / 4)
+        ts.append(e0.elapsed_time(e1) * 1e3 / 16)
     t = statistics.median(ts)
     extra = {"k": B * Hq * L * 4 + B * Hq * D * 4, "v": B * Hq * L * 4 + B * Hq * D * 4, "a": 0}[name]
     pb = (phys[0] if name == "k" else phys[1] if name == "v" else phys[0] + phys[1]) + extra
