@@ -165,6 +165,18 @@ int pkv_compress_codes(const pkv_layer_t* L, const uint16_t* k_new, const uint16
  * group when block % pack_size != 0.                        */
 int pkv_repack_plan(const uint16_t* codes, int32_t nsets, int32_t batch, int32_t heads, int32_t head_dim,
                     int32_t block, int32_t pack_size, int32_t repack, uint8_t* perm, void* stream);
+/* Graph-replayable flush (decode loop, default format, repack none): every
+ * sequence whose staging ring holds a full block (device nres[b] >= block)
+ * gets that block-set quantized, encoded and appended at the device block
+ * count nblk[b] and arena tail; nblk[b] += 1, nres[b] -= block.  Sequences
+ * with less staged do nothing.  Reads no host-side position, so
+ * pkv_stage_token + pkv_flush_staged + pkv_attention_decode (with nblocks
+ * headroom, blocks past nblk[b] are skipped) is one CUDA graph for every
+ * step.  The arena must have room (PKV_FLAG_CAPACITY otherwise).  Scratch:
+ * pkv_flush_scratch_bytes(L) (look-back words, zeroed by the call).       */
+int64_t pkv_flush_scratch_bytes(const pkv_layer_t* L);
+int pkv_flush_staged(const pkv_layer_t* L, float rel_k, float rel_v, void* scratch, int64_t scratch_bytes,
+                     void* stream);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:
  * [B][ntok][H][D] fp16.  `staged` = tokens already staged per sequence
  * (host mirror of nres, < block); `nblocks_before` = blocks per sequence

@@ -65,6 +65,8 @@ _SIGS = {
                                   c_void_p]),
     "pkv_compress_tokens": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_int32, c_int32, c_int32, c_float, c_float,
                                       c_int32, c_void_p, c_int64, c_void_p]),
+    "pkv_flush_scratch_bytes": (c_int64, [POINTER(Layer)]),
+    "pkv_flush_staged": (c_int32, [POINTER(Layer), c_float, c_float, c_void_p, c_int64, c_void_p]),
     "pkv_fused_k_scores": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_void_p, c_int64, c_void_p]),
     "pkv_fused_v_scratch_bytes": (c_int64, [POINTER(Layer), c_int32, c_int32]),
     "pkv_fused_v_output": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_int64,

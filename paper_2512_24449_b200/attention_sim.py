@@ -17,7 +17,7 @@ from .kv_store import CompressedStore, ctypes_ref
 
 
 def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride: int = 0, scores=None,
-                             out=None) -> torch.Tensor:
+                             out=None, nblocks: int = None) -> torch.Tensor:
     """q [B, Hq, D] -> out [B, Hq, D].
 
     The 1/sqrt(d) scale is applied to the (small) query instead of the
@@ -29,7 +29,10 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     fused V.  score_stride (>= the token count) sizes the
     internal score rows; GraphedAttention passes room for the whole staging
     ring so one capture serves every residue length.  scores / out may be
-    preallocated (graph capture without allocations)."""
+    preallocated (graph capture without allocations).  nblocks (default: the
+    layer's block count) sizes the fused launches; a larger value leaves
+    headroom for blocks appended on the device later (GraphedDecodeLoop):
+    blocks past a sequence's device count are skipped."""
     q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
     ls = store[layer]
     B, H, D = store.batch, store.heads, store.head_dim
@@ -38,9 +41,10 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     Hq = int(q.shape[1])
     lib = N.lib()
     st = ls.struct()
-    need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(st), ls.nblk_h, Hq))
+    nb = ls.nblk_h if nblocks is None else int(nblocks)
+    need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(st), nb, Hq))
     if need > 0:
-        stride = max(ls.tokens, score_stride, 1)
+        stride = max(ls.tokens, nb * store.block + ls.nres_h, score_stride, 1)
         stride = (stride + 3) // 4 * 4
         if scores is None or scores.shape[-1] < stride:
             scores = torch.empty((B, Hq, stride), dtype=torch.float32, device=store.device)
@@ -49,7 +53,7 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
             out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
         if ls.a_scratch.numel() < need:
             ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=store.device)
-        N.check(lib.pkv_attention_decode(ctypes_ref(st), ls.nblk_h, N.ptr(q), Hq, N.ptr(scores), stride, N.ptr(out),
+        N.check(lib.pkv_attention_decode(ctypes_ref(st), nb, N.ptr(q), Hq, N.ptr(scores), stride, N.ptr(out),
                                          N.ptr(ls.a_scratch), int(ls.a_scratch.numel()), N.stream()),
                 "attention_decode")
         return out
@@ -219,6 +223,135 @@ class GraphedDecodeStep(_Captured):
             self._q = torch.zeros((B, q_heads, D), dtype=torch.float32, device=st.device)
             self._key = None
         return self._k, self._v, self._q
+
+
+class GraphedDecodeLoop:
+    """The serving decode loop over one or more layers as ONE CUDA-graph replay
+    per step.  For every layer the graph holds: the step's K/V token staged at
+    the device residue count (pkv_stage_token), a block completed on the device
+    (pkv_flush_staged: quantize, encode and append the staged block-set at the
+    device block count and arena tail when nres reaches 64), and attention
+    over everything including the new token (pkv_attention_decode sized for
+    `headroom` more blocks; blocks past a sequence's device count are skipped).
+    No launch reads a host-side position, so the same graph replays across
+    block completions (SPEC.md:365-373 append_token
+    attention_decode).  It is re-captured only when the headroom is used up
+    (every headroom * 64 tokens) or a buffer moves.  Default format, repack
+    "none" (GraphedDecodeStep serves the others).
+
+    step(k, v, q): k / v [layers, B, 1, H, D] (or [layers, B, H, D]) fp16,
+    q [layers, B, Hq, D] f32 -> out [layers, B, Hq, D] (a static buffer,
+    overwritten by the next step).  inputs() returns the static input buffers;
+    a caller that writes them in place and calls step() without arguments
+    skips the copies."""
+
+    def __init__(self, store: CompressedStore, q_heads: int, layers=None, headroom: int = 16):
+        self.store = store
+        self.layers = list(range(store.layers)) if layers is None else list(layers)
+        self.headroom = max(1, int(headroom))
+        B, H, D = store.batch, store.heads, store.head_dim
+        if q_heads % H:
+            raise E.ShapeMismatchError(f"q_heads must be a multiple of kv heads ({H})")
+        if store.repack != "none" or store.pack_size != 16 or store.head_dim != 128 or store.block != 64:
+            raise ValueError("GraphedDecodeLoop: default format with repack none only (use GraphedDecodeStep)")
+        n, dev = len(self.layers), store.device
+        self.k = torch.zeros((n, B, 1, H, D), dtype=torch.float16, device=dev)
+        self.v = torch.zeros_like(self.k)
+        self.q = torch.zeros((n, B, q_heads, D), dtype=torch.float32, device=dev)
+        self.out = torch.empty((n, B, q_heads, D), dtype=torch.float32, device=dev)
+        self._flush_scr = [None] * n
+        self._scores = [None] * n
+        self._cap = [0] * n
+        self._graph = None
+        self._key = None
+        self._pool = None
+        self.captures = 0
+
+    def inputs(self):
+        return self.k, self.v, self.q
+
+    def _state(self):
+        st = []
+        for l in self.layers:
+            ls = self.store[l]
+            st.append((ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(), ls.a_scratch.data_ptr(),
+                       ls.max_blocks))
+        return tuple(st)
+
+    def _prepare(self):
+        """Host side of a (re)capture: tables, arena and scratch for `headroom`
+        more block-sets per layer, allocated before the capture."""
+        o = self.store
+        B, Hq = o.batch, self.q.shape[2]
+        lib = N.lib()
+        for i, l in enumerate(self.layers):
+            ls = o[l]
+            ls._ensure(self.headroom)
+            self._cap[i] = ls.nblk_h + self.headroom
+            if ls.max_blocks < self._cap[i]:
+                ls._grow_tables(self._cap[i])
+            L = ls.struct()
+            fb = int(lib.pkv_flush_scratch_bytes(ctypes_ref(L)))
+            if self._flush_scr[i] is None or self._flush_scr[i].numel() < fb:
+                self._flush_scr[i] = torch.empty(fb, dtype=torch.uint8, device=o.device)
+            need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(L), self._cap[i], Hq))
+            if ls.a_scratch.numel() < need:
+                ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=o.device)
+            stride = (self._cap[i] * o.block + o.buffer + 3) // 4 * 4
+            if self._scores[i] is None or self._scores[i].shape[-1] < stride:
+                self._scores[i] = torch.empty((B, Hq, stride), dtype=torch.float32, device=o.device)
+
+    def _record(self, with_append: bool):
+        o = self.store
+        lib = N.lib()
+        for i, l in enumerate(self.layers):
+            ls = o[l]
+            L = ctypes_ref(ls.struct())
+            if with_append:
+                N.check(lib.pkv_stage_token(L, N.ptr(self.k[i]), N.ptr(self.v[i]), N.stream()), "stage_token")
+            N.check(lib.pkv_flush_staged(L, float(o.rel_scale_k), float(o.rel_scale_v), N.ptr(self._flush_scr[i]),
+                                         int(self._flush_scr[i].numel()), N.stream()), "flush_staged")
+            attention_decode_batched(o, l, self.q[i], scores=self._scores[i], out=self.out[i], nblocks=self._cap[i])
+
+    def _capture(self):
+        dev = torch.device(self.store.device)
+        self._prepare()
+        self._record(False)  # warm-up outside the capture: nothing staged, so the flush appends nothing
+        if self._pool is None:
+            self._pool = torch.cuda.graph_pool_handle()
+            self._side = torch.cuda.Stream(device=dev)
+        cur = torch.cuda.current_stream(dev)
+        self._side.wait_stream(cur)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(self._side):
+            g.capture_begin(pool=self._pool)
+            try:
+                self._record(True)
+            finally:
+                g.capture_end()
+        cur.wait_stream(self._side)
+        self._graph = g
+        self._key = self._state()
+        self.captures += 1
+
+    def step(self, k=None, v=None, q=None) -> torch.Tensor:
+        o = self.store
+        for dst, src in ((self.k, k), (self.v, v), (self.q, q)):
+            if src is not None and src.data_ptr() != dst.data_ptr():
+                dst.copy_(src.reshape(dst.shape), non_blocking=True)
+        # the graph covers blocks j < cap: re-capture once a flush could create block cap
+        need = any(o[l].nblk_h >= self._cap[i] for i, l in enumerate(self.layers))
+        if self._graph is None or need or self._state() != self._key:
+            self._capture()
+        self._graph.replay()
+        for l in self.layers:  # host mirrors follow the device (lockstep batch)
+            ls = o[l]
+            ls.nres_h += 1
+            if ls.nres_h == o.block:
+                ls.nres_h = 0
+                ls.nblk_h += 1
+                ls.tail_ub += 2 * o.batch * o.heads * ls.blk_max
+        return self.out
 
 
 def attention_decode(store: CompressedStore, layer: int, head: int, q) -> torch.Tensor:

@@ -191,3 +191,47 @@ def test_smoke_entry_runs_fast_kernels():
     N, _, _, _ = _mods()
     ge.smoke()
     assert N.last_path() == N.PATH_FAST
+
+
+def test_graphed_decode_loop_device_flush():
+    """GraphedDecodeLoop: stage + device-side block flush + attention for two
+    layers in one CUDA graph per step.  Block completions happen inside the
+    replayed graph (no re-capture per 64 tokens); the arena streams stay
+    bit-identical to eager appends and to the oracle, and every step's
+    attention matches the eager composition on a store built by
+    append_token (SPEC.md:365-373, 520-528)."""
+    N, _, F, CS = _mods()
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeLoop, attention_decode_batched
+    rng = np.random.default_rng(77)
+    B, H, G, D, Ly = 2, 2, 4, 128, 2
+    T0, steps = 100, 200
+    k = (rng.standard_normal((Ly, B, T0 + steps, H, D))).astype(np.float16)
+    v = (rng.standard_normal((Ly, B, T0 + steps, H, D))).astype(np.float16)
+    q = rng.standard_normal((steps, Ly, B, H * G, D)).astype(np.float32)
+    a = CS(Ly, H, D, batch=B, check=False)
+    r = CS(Ly, H, D, batch=B, check=False)
+    for l in range(Ly):
+        a.compress_batch(l, k[l, :, :T0], v[l, :, :T0])
+        r.compress_batch(l, k[l, :, :T0], v[l, :, :T0])
+    loop = GraphedDecodeLoop(a, H * G, headroom=2)   # headroom 2: re-captures every 128 tokens
+    kd, vd, qd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    worst = 0.0
+    for t in range(steps):
+        out = loop.step(kd[:, :, T0 + t:T0 + t + 1], vd[:, :, T0 + t:T0 + t + 1], qd[t]).clone()
+        for l in range(Ly):
+            r.append_token(l, kd[l, :, T0 + t], vd[l, :, T0 + t])
+            ref = attention_decode_batched(r, l, qd[t, l])
+            e = float((out[l] - ref).abs().max() / ref.abs().max())
+            worst = max(worst, e)
+    assert worst <= 1e-5, worst
+    torch.cuda.synchronize()
+    a.check_errors()
+    assert loop.captures <= steps // 128 + 2, loop.captures
+    for l in range(Ly):
+        assert a[l].nblk_h == r[l].nblk_h and a[l].nres_h == r[l].nres_h
+        assert int(a[l].nblk[0].item()) == r[l].nblk_h and int(a[l].nres[0].item()) == r[l].nres_h
+        for b in range(B):
+            assert a[l].stream_bytes(b) == r[l].stream_bytes(b), f"layer {l} seq {b}: stream differs"
+    ref = O.OracleStore(1, H, D)
+    ref.compress_batch(0, k[1, 1], v[1, 1])
+    assert a[1].stream_bytes(1) == ref.layer_stream(0)
