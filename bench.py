@@ -42,8 +42,11 @@ CONFIGS = {
     # key: (batch, kv_heads, q_heads, head_dim, tokens, description)
     "A": (1, 32, 32, 128, 4096, "Llama-2-7B single layer, MHA 32x128, 4K tokens, batch 1"),
     "B": (8, 8, 32, 128, 32768, "Llama-3-8B GQA (8 kv / 32 q heads), 32K context, batch 8, 1 layer"),
-    "D": (8, 52, 52, 128, 32768, "LLaMA-30B shape (52 heads x 128), 32K context, batch 8, 1 layer"),
+    "D": (8, 52, 52, 128, 32768, "LLaMA-30B shape (52 heads x 128), 32K context, batch 8, 15 layers (~105 GB fp16 "
+                                 "K+V)"),
     "E": (16, 8, 64, 128, 131072, "Llama-3-70B GQA (8 kv / 64 q heads), 128K context, batch 16, 1 layer"),
+    "C": (1, 40, 40, 128, 6144, "Llama-2-13B streaming decode: 40 layers x 40 heads x 128, batch 1, 2K prefill "
+                                "then 4K append+attend steps"),
 }
 
 
@@ -266,7 +269,7 @@ def compressor_bench(cfg, rank, T=4096, appends=128):
     appends (staging copies; every 64th flushes a block-set).  CUDA-event timed;
     the fp16 inputs are resident in HBM."""
     import torch
-    from paper_2512_24449_b200.attention_sim import GraphedDecodeStep
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeLoop
     from paper_2512_24449_b200.kv_store import CompressedStore
     from paper_2512_24449_b200.tensor_model import gauss_outlier
     B, Hkv, Hq, D, L, _ = cfg
@@ -290,17 +293,17 @@ def compressor_bench(cfg, rank, T=4096, appends=128):
         for t in range(appends):
             st.append_token(0, kk[:, t], vv[:, t])
         e2.record()
-        # a serving decode step: append this step's K/V token, then attention
-        # through the captured graph (replays while only the residue grows)
-        dstep = GraphedDecodeStep(st, 0)
-        qd = torch.randn((B, Hq, D), device="cuda")
-        ktok = [kk[:, t].contiguous() for t in range(appends)]
-        vtok = [vv[:, t].contiguous() for t in range(appends)]
-        dstep(ktok[0], vtok[0], qd)  # first capture (module loading, warm-up) untimed
+        # a serving decode step: append this step's K/V token (a block completes
+        # every 64 steps, on the device), then attention -- one graph replay
+        dstep = GraphedDecodeLoop(st, Hq, layers=[0], headroom=16)
+        qd = torch.randn((1, B, Hq, D), device="cuda")
+        ktok = [kk[:, t].reshape(1, B, 1, Hkv, D).contiguous() for t in range(appends)]
+        vtok = [vv[:, t].reshape(1, B, 1, Hkv, D).contiguous() for t in range(appends)]
+        dstep.step(ktok[0], vtok[0], qd)  # first capture (module loading, warm-up) untimed
         e3, e4 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e3.record()
         for t in range(1, appends):
-            dstep(ktok[t], vtok[t], qd)
+            dstep.step(ktok[t], vtok[t], qd)
         e4.record()
         torch.cuda.synchronize()
         pre_ms, app_ms, step_ms = e0.elapsed_time(e1), e1.elapsed_time(e2), e3.elapsed_time(e4)
@@ -319,8 +322,8 @@ def compressor_bench(cfg, rank, T=4096, appends=128):
            "decode_step_context": T + 2 * appends,
            "note": f"batch {B} x {Hkv} kv-heads x {D}, K and V, repack none; appends include "
                    f"{appends // 64} block-set flushes (host-driven launches); arena reserved before the "
-                   f"timed prefill; decode_step = attention_sim.GraphedDecodeStep (stage token + "
-                   f"attention in one graph replay; block completions run the compressor and re-capture) at "
+                   f"timed prefill; decode_step = attention_sim.GraphedDecodeLoop (stage token + device-side "
+                   f"block flush + attention in one graph replay; no re-capture at block completions) at "
                    f"~{T // 1024}K context"}
     del st
     torch.cuda.empty_cache()
@@ -377,30 +380,38 @@ def cublas_baseline(cfg, rank, reps=10):
     return res
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-cublas", action="store_true")
-    args = ap.parse_args()
-    args.warmup = max(3, args.warmup)
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        return
+# config -> (layers, split, scaling) of the decode-step bench (BASELINE.json configs;
+# SURVEY §8 config key): B weak-scales by batch (the driver's default, N = 1 is the
+# metric's config), D is the 15-layer ~105 GB LLaMA-30B variant with a strong batch
+# split, E is Llama-3-70B head-sharded as strong scaling; C is the streaming decode
+# (run_streaming) and A the reference's CPU-runnable case.
+MODES = {"A": (1, "batch", "weak"), "B": (1, "batch", "weak"), "D": (15, "batch", "strong"),
+         "E": (1, "head", "strong")}
 
-    import numpy as np
+
+def build_local_store(cfg, part, layers, rank, chunk=4096):
+    """This rank's (sequence, kv-head) units of every layer, synthetic KV of the
+    config shape (tensor_model.gauss_outlier: 4 / 1 outlier channels per kv head)."""
+    import torch
+    from paper_2512_24449_b200.kv_store import CompressedStore
+    from paper_2512_24449_b200.tensor_model import gauss_outlier
+    B, Hkv, Hq, D, L, _ = cfg
+    Bl, Hl = part.local_batch, part.local_heads
+    st = CompressedStore(layers, Hl, D, batch=Bl, max_tokens=L, check=False)
+    for l in range(layers):
+        for t0 in range(0, L, chunk):
+            T = min(chunk, L - t0)
+            seed = 17 + 7919 * rank + 104729 * l + t0
+            st.compress_batch(l, gauss_outlier((Bl, T, Hl, D), n_outlier=4, seed=seed),
+                              gauss_outlier((Bl, T, Hl, D), n_outlier=1, seed=seed + 12))
+    torch.cuda.synchronize()
+    st.check_errors()
+    return st
+
+
+def init_dist(local, world, backend):
     import torch
     import torch.distributed as dist
-    # PKV_BENCH_BACKEND=gloo (structural test of the N > 1 path with several ranks on
-    # one device); production runs use NCCL, one rank per GPU
-    backend = os.environ.get("PKV_BENCH_BACKEND", "nccl")
     ndev = torch.cuda.device_count()
     if backend == "nccl":
         if local >= ndev:  # one NCCL rank per GPU: never two ranks on one device
@@ -420,6 +431,163 @@ def main():
                                         "backend": dist.get_backend(), "device": f"cuda:{local}",
                                         "gpu": torch.cuda.get_device_name(local),
                                         "nranks_ok": int(probe.item()) == world}}), file=sys.stderr, flush=True)
+    return local
+
+
+def max_over_ranks(vals, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def run_streaming(args, rank, world, local, backend):
+    """Config C (BASELINE.json configs[2]): streaming decode on the Llama-2-13B
+    shape -- 40 layers x 40 heads x 128, batch 1, a 2K-token prefill, then 4K
+    decode steps; each step appends one K/V token to every layer (SPEC.md:365-373,
+    a block completes every 64 steps) and attends with that layer's query over
+    everything so far.  One CUDA graph per step holds all 40
+    layers' stage + device-side flush + fused attention (GraphedDecodeLoop).
+    W warm-up decode steps are untimed; the remaining appends are timed
+    (tokens/s).  At N > 1 every rank runs its own replica (the stream is one
+    sequence: it does not shard)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeLoop
+    from paper_2512_24449_b200.kv_store import CompressedStore
+    from paper_2512_24449_b200.tensor_model import gauss_outlier
+    Ly, H, D, T0, NT = 40, 40, 128, 2048, args.stream_steps
+    B, Hq = 1, 40
+    st = CompressedStore(Ly, H, D, batch=B, max_tokens=T0 + NT, check=False)
+    for l in range(Ly):
+        st.compress_batch(l, gauss_outlier((B, T0, H, D), n_outlier=4, seed=11 + l + 97 * rank),
+                          gauss_outlier((B, T0, H, D), n_outlier=1, seed=13 + l + 97 * rank))
+    loop = GraphedDecodeLoop(st, Hq, headroom=16)
+    kin, vin, qin = loop.inputs()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5 + rank)
+    # the decode tokens are generated 64 steps at a time into a ring (what a model
+    # would produce); q is a fixed set of 16 per-layer queries cycled over the steps
+    qs = torch.randn((16, Ly, B, Hq, D), device="cuda", generator=g)
+    kr = torch.empty((64, Ly, B, 1, H, D), dtype=torch.float16, device="cuda")
+    vr = torch.empty_like(kr)
+
+    def refill(t):
+        kr.copy_(gauss_outlier((64, Ly, B, 1, H, D), n_outlier=4, seed=1000 + t).view_as(kr))
+        vr.copy_(gauss_outlier((64, Ly, B, 1, H, D), n_outlier=1, seed=2000 + t).view_as(vr))
+
+    W = min(args.warmup, NT - 1)
+    t = 0
+    refill(0)
+    while t < W:  # warm-up decode steps (first capture, module loading): untimed appends
+        loop.step(kr[t % 64], vr[t % 64], qs[t % 16])
+        t += 1
+        if t % 64 == 0:
+            refill(t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx0 = T0 + t
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record()
+        while t < NT:
+            if t % 64 == 0:
+                refill(t)  # inside the timed region: the model would produce these tokens anyway
+            loop.step(kr[t % 64], vr[t % 64], qs[t % 16])
+            t += 1
+        e1.record()
+        torch.cuda.synchronize()
+    timed = NT - W
+    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks([ms], world)[0]
+    # bytes: every step reads the whole cache of every layer once for K and once for V
+    logical = sum(Ly * 2 * B * H * (ctx0 + i + 1) * D * 2 for i in range(timed))
+    value = world * logical / (ms * 1e-3) / 1e9
+    tok_s = world * timed / (ms * 1e-3)
+    # e2e through the public API from HOST buffers: pinned k, v, q per step
+    # copied into the loop, the per-layer outputs copied back
+    E2E = min(256, max(64, args.steps))
+    kh = kr[:1].expand(E2E, *kr.shape[1:]).cpu().pin_memory()
+    vh = vr[:1].expand(E2E, *vr.shape[1:]).cpu().pin_memory()
+    qh = qs[:1].expand(E2E, *qs.shape[1:]).cpu().pin_memory()
+    oh = torch.empty((Ly, B, Hq, D)).pin_memory()
+    st2 = CompressedStore(Ly, H, D, batch=B, max_tokens=T0 + E2E + 64, check=False)
+    for l in range(Ly):
+        st2.compress_batch(l, gauss_outlier((B, T0, H, D), n_outlier=4, seed=11 + l),
+                           gauss_outlier((B, T0, H, D), n_outlier=1, seed=13 + l))
+    loop2 = GraphedDecodeLoop(st2, Hq, headroom=16)
+    loop2.step(kh[0].cuda(), vh[0].cuda(), qh[0].cuda())
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for i in range(1, E2E):
+        o = loop2.step(kh[i], vh[i], qh[i])  # pinned host -> the graph's input buffers
+        oh.copy_(o, non_blocking=True)
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks([a0.elapsed_time(a1) / (E2E - 1)], world)[0]
+    e2e_logical = Ly * 2 * B * H * (T0 + E2E // 2) * D * 2
+    st.check_errors()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": timed,
+            "warmup": W, "ms_per_step": round(ms / timed, 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8->f32", "data": "synthetic gaussian + outlier channels (BASELINE.md §3)",
+            "config": {"workload": f"config C: {CONFIGS['C'][-1]}", "layers": Ly, "kv_heads": H, "q_heads": Hq,
+                       "head_dim": D, "batch": B, "prefill_tokens": T0, "decode_steps": NT,
+                       "context_timed": [ctx0, T0 + NT], "rel_k": 0.1, "rel_v": 0.2, "pack_size": 16,
+                       "block": 64, "repack": "none",
+                       "parallelism": f"replicas x{world} (one stream per GPU; the path does not shard)",
+                       "l2": "per-step working set (40 layers of compressed K+V) exceeds the 126 MB L2"},
+            "tokens_per_s": round(tok_s, 1), "us_per_token": round(ms * 1e3 / timed, 2),
+            "step": ("GraphedDecodeLoop: one CUDA-graph replay per token: for each of the 40 layers "
+                     "pkv_stage_token + pkv_flush_staged (device-side block completion) + pkv_attention_decode; "
+                     f"re-captures {loop.captures} (every {loop.headroom * 64} tokens)"),
+            "e2e": {"value": round(world * e2e_logical / (e2e_ms * 1e-3) / 1e9, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": Ly * B * (2 * H * D * 2 + Hq * D * 4),
+                    "d2h_bytes_per_step": Ly * B * Hq * D * 4,
+                    "tokens_per_s": round(world * 1e3 / e2e_ms, 1), "ms_per_step": round(e2e_ms, 5),
+                    "path": "GraphedDecodeLoop.step from pinned host k/v/q, output copied back each step"},
+            "gpu_launches": timed * Ly * 6, "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
+    ap.add_argument("--stream-steps", type=int, default=4096, help="config C: decode steps after the prefill")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    # PKV_BENCH_BACKEND=gloo (structural test of the N > 1 path with several ranks on
+    # one device); production runs use NCCL, one rank per GPU
+    backend = os.environ.get("PKV_BENCH_BACKEND", "nccl")
+    local = init_dist(local, world, backend)
+    if args.config == "C":
+        run_streaming(args, rank, world, local, backend)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     def gather_into(dst, src):
         if backend == "nccl":
@@ -432,60 +600,69 @@ def main():
     cfg = CONFIGS[args.config]
     B, Hkv, Hq, D, L, desc = cfg
     G = Hq // Hkv
-    # weak scaling: the job holds B sequences per GPU, sharded by sequence
-    part = S.plan_partition(B * world, Hkv, world, rank, prefer="batch")
-    st = build_store(cfg, rank)
-    dec = S.ShardedDecoder(part, S.cuda_local_attention(st), Hq, D)
+    layers, split, scaling = MODES[args.config]
+    if scaling == "weak":  # the job holds B sequences per GPU, sharded by sequence
+        part = S.plan_partition(B * world, Hkv, world, rank, prefer="batch")
+    else:                  # the config's fixed job, split `split`-wise over the ranks
+        part = S.plan_partition(B, Hkv, world, rank, prefer=split)
+    Bl, Hl = part.local_batch, part.local_heads
+    Hql = Hl * G
+    st = build_local_store(cfg, part, layers, rank)
     ls = st[0]
-    _, ln, _ = ls.tables()
-    phys_k = int(ln[0].astype(np.int64).sum())
-    phys_v = int(ln[1].astype(np.int64).sum())
-    nblocks_k = int(ln[0].size)
-    logical_kind = B * Hkv * L * D * 2
+    tabs = [st[l].tables()[1] for l in range(layers)]
+    phys_k = sum(int(t[0].astype(np.int64).sum()) for t in tabs)
+    phys_v = sum(int(t[1].astype(np.int64).sum()) for t in tabs)
+    nblocks_k = sum(int(t[0].size) for t in tabs)
+    logical_kind = layers * Bl * Hl * L * D * 2          # per rank, all layers
     cr_k_wire, cr_v_wire = logical_kind / phys_k, logical_kind / phys_v
-    cr_k = B * Hkv * (L // 64) * 64 * D * 2 / (phys_k - 8 * nblocks_k)
-    cr_v = B * Hkv * (L // 64) * 64 * D * 2 / (phys_v - 8 * nblocks_k)
-    res_bytes = B * Hkv * ls.nres_h * D * 2
-    alg_k = phys_k + res_bytes + B * Hq * D * 4 + B * Hq * L * 4
-    alg_v = phys_v + res_bytes + B * Hq * L * 4 + B * Hq * D * 4
+    full = layers * Bl * Hl * (L // 64) * 64 * D * 2
+    cr_k = full / (phys_k - 8 * nblocks_k)
+    cr_v = full / (phys_v - 8 * nblocks_k)
+    res_bytes = layers * Bl * Hl * ls.nres_h * D * 2
+    alg_k = (phys_k + res_bytes) / layers + Bl * Hql * D * 4 + Bl * Hql * L * 4   # per launch (one layer)
+    alg_v = (phys_v + res_bytes) / layers + Bl * Hql * L * 4 + Bl * Hql * D * 4
 
-    # HBM held by the compressed layer (SPEC.md:499 reports peak allocation): the arena's
-    # used bytes, its reserved capacity and the tables / staging next to fp16 K+V
-    tail = int(ls.tail.item())
-    side = sum(t.numel() * t.element_size() for t in (ls.blk_off, ls.blk_len, ls.perm, ls.nblk, ls.nres, ls.stage))
-    mem = {"fp16_kv_bytes": 2 * logical_kind, "arena_used_bytes": tail, "arena_capacity_bytes": ls.capacity,
+    # HBM held by the compressed layers (SPEC.md:499 reports peak allocation)
+    tail = sum(int(st[l].tail.item()) for l in range(layers))
+    side = sum(t.numel() * t.element_size() for l in range(layers)
+               for t in (st[l].blk_off, st[l].blk_len, st[l].perm, st[l].nblk, st[l].nres, st[l].stage))
+    mem = {"fp16_kv_bytes": 2 * logical_kind, "arena_used_bytes": tail,
+           "arena_capacity_bytes": sum(st[l].capacity for l in range(layers)),
            "tables_and_staging_bytes": side, "hbm_ratio_vs_fp16": round(2 * logical_kind / (tail + side), 3),
            "peak_allocated_bytes_after_build": int(torch.cuda.max_memory_allocated()),
            "note": "arena capacity is geometric-growth reservation; CompressedStore.shrink_to_fit() releases it"}
-    q = torch.randn((B, Hq, D), device="cuda")
-    scores = torch.empty((B, Hq, L), device="cuda")
-    out = torch.empty((B, Hq, D), device="cuda")
-    F.fused_k_scores_batched(st, 0, q, out=scores)
+    qs = torch.randn((layers, Bl, Hql, D), device="cuda")
+    scores = torch.empty((Bl, Hql, L), device="cuda")
+    out = torch.empty((layers, Bl, Hql, D), device="cuda")
+    F.fused_k_scores_batched(st, 0, qs[0], out=scores)
     w = torch.softmax(scores / math.sqrt(D), -1).contiguous()
-    gathered = torch.empty((world * B, Hq, D), device="cuda") if world > 1 else None
+    gathered = torch.empty((world * layers * Bl, Hql, D), device="cuda") if world > 1 else None
 
-    def step():
-        F.fused_k_scores_batched(st, 0, q, out=scores)
-        F.fused_v_output_batched(st, 0, w, out=out)
-        if world > 1:
-            gather_into(gathered, out)
+    def run_k():
+        for l in range(layers):
+            F.fused_k_scores_batched(st, l, qs[l], out=scores)
+
+    def run_v():
+        for l in range(layers):
+            F.fused_v_output_batched(st, l, w, out=out[l])
 
     for _ in range(args.warmup):
-        step()
-    # the timed launches replay CUDA graphs of the fused K and V calls (a decode
-    # step's launches without Python launch overhead, as GraphedAttention runs)
+        run_k()
+        run_v()
+    # the timed launches replay CUDA graphs of the fused K and V calls of every
+    # layer (a decode step's launches without Python launch overhead)
     gk, gv = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     with torch.cuda.graph(gk):
-        F.fused_k_scores_batched(st, 0, q, out=scores)
+        run_k()
     with torch.cuda.graph(gv):
-        F.fused_v_output_batched(st, 0, w, out=out)
+        run_v()
     for _ in range(args.warmup):
         gk.replay()
         gv.replay()
     K = args.steps
     # working sets below ~L2 size (config A) are flushed between timed steps by
     # writing 256 MB; ms_per_step is then the sum of the K and V launch times
-    l2_flush = phys_k + phys_v + 2 * B * Hq * L * 4 < 160 * 2 ** 20
+    l2_flush = phys_k + phys_v + 2 * Bl * Hql * L * 4 < 160 * 2 ** 20
     flush_buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda") if l2_flush else None
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     if world > 1:
@@ -506,7 +683,7 @@ def main():
             gv.replay()
             evs[i][2].record()
             if world > 1:
-                gather_into(gathered, out)
+                gather_into(gathered, out.view(-1, Hql, D))
         e_end.record()
         torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
@@ -515,22 +692,21 @@ def main():
     ms = e_start.elapsed_time(e_end) / K
     k_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     v_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
-    t = torch.tensor([ms, k_ms, v_ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, k_ms, v_ms = (float(x) for x in t.tolist())
+    ms, k_ms, v_ms = max_over_ranks([ms, k_ms, v_ms], world)
     if l2_flush:
         ms = k_ms + v_ms
     value = world * 2 * logical_kind / (ms * 1e-3) / 1e9
 
     # ---- e2e through the public API: host q (this rank's shard) -> sharded
-    # decode (fused K, softmax, fused V, NCCL all-gather) -> host output
-    q_host = torch.randn((B, Hq, D)).pin_memory()
-    out_host = torch.empty((world * B, Hq, D)).pin_memory()
+    # decode (fused K, softmax, fused V, NCCL all-gather) per layer -> host output
+    decs = [S.ShardedDecoder(part, S.cuda_local_attention(st, l), Hq, D) for l in range(layers)]
+    q_host = torch.randn((layers, Bl, Hql, D)).pin_memory()
+    out_host = torch.empty((layers, world * Bl * Hql * D)).pin_memory()
 
     def e2e_step():
-        o = dec.step(q_host)  # pinned host q: copied straight into the graph's input buffer
-        out_host.copy_(o, non_blocking=True)
+        for l in range(layers):
+            o = decs[l].step(q_host[l])  # pinned host q: copied straight into the graph's input buffer
+            out_host[l].copy_(o.reshape(-1), non_blocking=True)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -543,15 +719,12 @@ def main():
         e2e_step()
     a1.record()
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([a0.elapsed_time(a1) / K], device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
+    e2e_ms = max_over_ranks([a0.elapsed_time(a1) / K], world)[0]
     e2e_value = world * 2 * logical_kind / (e2e_ms * 1e-3) / 1e9
 
     peak, peak_src = load_peaks()
     dom = "k" if k_ms >= v_ms else "v"
-    dom_ms = k_ms if dom == "k" else v_ms
+    dom_ms = (k_ms if dom == "k" else v_ms) / layers          # one launch (one layer)
     alg = alg_k if dom == "k" else alg_v
     achieved = alg / (dom_ms * 1e-3) / 1e9
     traffic = load_traffic().get(f"{args.config}_{dom}")
@@ -559,8 +732,8 @@ def main():
     cub = None
     if not args.no_cublas:
         del scores
-        cub = cublas_baseline(cfg, rank)
-    comp = compressor_bench(cfg, rank) if not args.no_cublas else None
+        cub = cublas_baseline((Bl, Hl, Hql, D, L, desc), rank)
+    comp = compressor_bench(cfg, rank) if not args.no_cublas and args.config in ("A", "B") else None
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ncores = len(os.sched_getaffinity(0))
@@ -569,58 +742,62 @@ def main():
                              "and cost O(tokens)")
         cb["parity"] = parity_sample(cfg)
     if rank == 0:
+        kind_layer = logical_kind / layers
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "u8->f32", "data": "synthetic gaussian + outlier channels (BASELINE.md §3)",
-            "config": {"workload": f"config {args.config}: {desc}", "batch": B, "kv_heads": Hkv, "q_heads": Hq,
-                       "head_dim": D, "tokens": L, "layers": 1, "rel_k": 0.1, "rel_v": 0.2, "pack_size": 16,
-                       "block": 64, "repack": "none", "parallelism": f"(batch, kv-head) shards x{world} ({part.mode} split), "
+            "config": {"workload": f"config {args.config}: {desc}", "batch": B if scaling == "strong" else B * world,
+                       "kv_heads": Hkv, "q_heads": Hq, "head_dim": D, "tokens": L, "layers": layers,
+                       "per_rank": {"batch": Bl, "kv_heads": Hl, "q_heads": Hql},
+                       "rel_k": 0.1, "rel_v": 0.2, "pack_size": 16, "block": 64, "repack": "none",
+                       "parallelism": f"(batch, kv-head) shards x{world} ({part.mode} split, {scaling} scaling), "
                                       f"{'NCCL' if backend == 'nccl' else backend} all-gather of outputs",
-                       "global_batch": B * world,
+                       "global_batch": B if scaling == "strong" else B * world,
                        "l2": ("working set below L2: 256 MB written between timed steps, ms_per_step = K + V "
                               "launch times" if l2_flush else
                               "per-step working set (compressed K+V blocks) exceeds the 126 MB L2")},
             "compression_ratio": {"k": round(cr_k, 4), "v": round(cr_v, 4), "k_wire": round(cr_k_wire, 4),
                                   "v_wire": round(cr_v_wire, 4)},
-            "kernels": {"fused_k_us": round(k_ms * 1e3, 2), "fused_v_us": round(v_ms * 1e3, 2),
-                        "fused_k_gbs_equiv": round(logical_kind / (k_ms * 1e-3) / 1e9, 1),
-                        "fused_v_gbs_equiv": round(logical_kind / (v_ms * 1e-3) / 1e9, 1),
-                        "fused_k_gbs_physical": round(alg_k / (k_ms * 1e-3) / 1e9, 1),
-                        "fused_v_gbs_physical": round(alg_v / (v_ms * 1e-3) / 1e9, 1)},
+            "kernels": {"fused_k_us": round(k_ms * 1e3 / layers, 2), "fused_v_us": round(v_ms * 1e3 / layers, 2),
+                        "per": "one launch = one layer on this rank's units",
+                        "fused_k_gbs_equiv": round(kind_layer / (k_ms / layers * 1e-3) / 1e9, 1),
+                        "fused_v_gbs_equiv": round(kind_layer / (v_ms / layers * 1e-3) / 1e9, 1),
+                        "fused_k_gbs_physical": round(alg_k / (k_ms / layers * 1e-3) / 1e9, 1),
+                        "fused_v_gbs_physical": round(alg_v / (v_ms / layers * 1e-3) / 1e9, 1)},
             "roofline": {"bound": "hbm", "kernel": f"fused_{dom}", "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "algorithmic_bytes_per_launch": alg,
+                         "traffic": traffic, "algorithmic_bytes_per_launch": int(alg),
                          "frac_vs_nominal_8000_gbs": round(achieved / 8000.0, 4)},
-            "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": B * Hq * D * 4,
-                    "d2h_bytes_per_step": world * B * Hq * D * 4,
-                    "path": "sharding.ShardedDecoder.step (public API) on the pinned host q shard: H2D straight "
-                            "into the graph's input buffer, one CUDA-graph replay of fused K + softmax + fused V "
-                            "(attention_sim.GraphedAttention), NCCL all-gather of per-head outputs, D2H out",
+            "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": layers * Bl * Hql * D * 4,
+                    "d2h_bytes_per_step": layers * world * Bl * Hql * D * 4,
+                    "path": "sharding.ShardedDecoder.step (public API) per layer on the pinned host q shard: H2D "
+                            "straight into the graph's input buffer, one CUDA-graph replay of fused K + softmax + "
+                            "fused V (attention_sim.GraphedAttention), all-gather of per-head outputs, D2H out",
                     "ms_per_step": round(e2e_ms, 5)},
             "memory": mem,
             # scaling with and without the all-gather -- the same
             # whole-job metric from the K + V launch times alone (max over ranks)
             "value_without_collective": round(world * 2 * logical_kind / ((k_ms + v_ms) * 1e-3) / 1e9, 2),
-            "gpu_launches": 3 * K,
+            "gpu_launches": 3 * K * layers,
             "clocks": sampler.summary(),
         }
         if cub:
             line["cublas"] = {"k_us": round(cub["k_us"], 2), "k_transposed_us": round(cub["k_t_us"], 2),
                               "v_us": round(cub["v_us"], 2), "v_transposed_us": round(cub["v_t_us"], 2),
                               "k_best_us": round(cub["k_best_us"], 2), "v_best_us": round(cub["v_best_us"], 2),
-                              "k_gbs_equiv": round(logical_kind / (cub["k_best_us"] * 1e-6) / 1e9, 1),
-                              "v_gbs_equiv": round(logical_kind / (cub["v_best_us"] * 1e-6) / 1e9, 1),
-                              "speedup_k": round(cub["k_best_us"] / (k_ms * 1e3), 3),
-                              "speedup_v": round(cub["v_best_us"] / (v_ms * 1e3), 3),
+                              "k_gbs_equiv": round(kind_layer / (cub["k_best_us"] * 1e-6) / 1e9, 1),
+                              "v_gbs_equiv": round(kind_layer / (cub["v_best_us"] * 1e-6) / 1e9, 1),
+                              "speedup_k": round(cub["k_best_us"] / (k_ms * 1e3 / layers), 3),
+                              "speedup_v": round(cub["v_best_us"] / (v_ms * 1e3 / layers), 3),
                               "fp16_gemv_at_hbm_peak_us": {"k": round(cub["k_fp16_at_hbm_peak_us"], 2),
                                                            "v": round(cub["v_fp16_at_hbm_peak_us"], 2)},
                               "speedup_vs_fp16_at_hbm_peak": {
-                                  "k": round(cub["k_fp16_at_hbm_peak_us"] / (k_ms * 1e3), 3),
-                                  "v": round(cub["v_fp16_at_hbm_peak_us"] / (v_ms * 1e3), 3)},
-                              "note": "best of both operand orientations of torch.matmul fp16 (cuBLAS), and "
-                                      "an ideal fp16 GEMV reading the uncompressed cache at the measured HBM "
-                                      "peak"}
+                                  "k": round(cub["k_fp16_at_hbm_peak_us"] / (k_ms * 1e3 / layers), 3),
+                                  "v": round(cub["v_fp16_at_hbm_peak_us"] / (v_ms * 1e3 / layers), 3)},
+                              "note": "per layer; best of both operand orientations of torch.matmul fp16 "
+                                      "(cuBLAS), and an ideal fp16 GEMV reading the uncompressed cache at the "
+                                      "measured HBM peak"}
         if comp:
             line["compressor"] = comp
         if cb:
