@@ -101,6 +101,7 @@ int pkv_version(void);
 #define PKV_PATH_NONE 0
 #define PKV_PATH_FAST 1
 #define PKV_PATH_GENERIC 2
+#define PKV_PATH_SINGLE 3 /* pkv_attention_decode single pass (attn_fused_kernel) */
 int pkv_last_path(void);
 
 /* --- quantizer -------------------------------------- */
@@ -210,11 +211,18 @@ int pkv_fused_v_output(const pkv_layer_t* L, int32_t nblocks, const float* w, in
 /* Scratch bytes for pkv_attention_decode (0: format not fused, -1: bad args). */
 int64_t pkv_attention_scratch_bytes(const pkv_layer_t* L, int32_t nblocks, int32_t q_heads);
 /* out[b][hq] = softmax(scores[b][hq]) . deq(V[b, hq/G]) with
- * scores = deq(K)·q written to `scores` ([B][q_heads][score_stride] f32, the
- * caller pre-scales q by 1/sqrt(d)).  Three launches: fused K (also records
- * per-slot score maxima), fused V on exp(s - M) with the row maximum M (no
- * softmax pass, no rescaling), normalising finalize.  Default format only
- * (pack 16, head_dim 128, block 64, G <= 8); else PKV_E_ARG.            */
+ * scores = deq(K)·q (the caller pre-scales q by 1/sqrt(d)).
+ *   scores == NULL: single pass (attn_fused_kernel, §8 f1): one launch
+ *     decodes K and V block by block with an online softmax per query head
+ *     and merges the per-warp partials in a fixed order (deterministic); no
+ *     score row ever reaches HBM.  score_stride is ignored.
+ *   scores != NULL ([B][q_heads][score_stride] f32): the scores are also
+ *     returned.  Three launches: fused K (also records per-slot score
+ *     maxima), fused V on exp(s - M) with the row maximum M, normalising
+ *     finalize.
+ * q, out and scratch 16-byte aligned.  Default format only (pack 16,
+ * head_dim 128, block 64, G <= 8); else PKV_E_ARG.  Blocks past a
+ * sequence's device count nblk[b] (nblocks headroom) are skipped.      */
 int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const float* q, int32_t q_heads, float* scores,
                          int64_t score_stride, float* out, void* scratch, int64_t scratch_bytes, void* stream);
 

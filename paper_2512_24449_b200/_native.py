@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 PKV_OK, PKV_E_SHAPE, PKV_E_NONFINITE, PKV_E_WIDTH, PKV_E_MALFORMED = 0, 1, 2, 3, 4
 PKV_E_INDEX, PKV_E_ARG, PKV_E_CUDA, PKV_E_CAPACITY = 5, 6, 7, 8
 FLAG_NONFINITE, FLAG_WIDTH, FLAG_MALFORMED, FLAG_CAPACITY, FLAG_SHAPE = 1, 2, 4, 8, 16
-PATH_NONE, PATH_FAST, PATH_GENERIC = 0, 1, 2
+PATH_NONE, PATH_FAST, PATH_GENERIC, PATH_SINGLE = 0, 1, 2, 3
 REPACK = {"none": 0, "greedy": 1, "v_median": 2}
 REPACK_EXTERNAL = 3
 
@@ -160,7 +160,7 @@ def raise_flags(flags: int, what: str = ""):
 
 
 def last_path() -> int:
-    """PATH_FAST / PATH_GENERIC: kernel family of this thread's last fused call."""
+    """PATH_FAST / PATH_GENERIC / PATH_SINGLE: kernel family of this thread's last fused call."""
     return int(load().pkv_last_path())
 
 

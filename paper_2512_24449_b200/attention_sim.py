@@ -17,7 +17,7 @@ from .kv_store import CompressedStore, ctypes_ref
 
 
 def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride: int = 0, scores=None,
-                             out=None, nblocks: int = None) -> torch.Tensor:
+                             out=None, nblocks: int = None, single_pass: bool = None) -> torch.Tensor:
     """q [B, Hq, D] -> out [B, Hq, D].
 
     The 1/sqrt(d) scale is applied to the (small) query instead of the
@@ -32,7 +32,13 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     preallocated (graph capture without allocations).  nblocks (default: the
     layer's block count) sizes the fused launches; a larger value leaves
     headroom for blocks appended on the device later (GraphedDecodeLoop):
-    blocks past a sequence's device count are skipped."""
+    blocks past a sequence's device count are skipped.
+
+    single_pass (default: True unless `scores` is given): the default format
+    runs ONE launch (attn_fused_kernel: K, online softmax and V block by
+    block, deterministic merge of the per-warp partials) and no score row
+    reaches HBM; False keeps the three-launch path, which also fills
+    `scores`."""
     q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
     ls = store[layer]
     B, H, D = store.batch, store.heads, store.head_dim
@@ -43,6 +49,17 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     st = ls.struct()
     nb = ls.nblk_h if nblocks is None else int(nblocks)
     need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(st), nb, Hq))
+    if single_pass is None:
+        single_pass = scores is None
+    if need > 0 and single_pass:
+        if out is None:
+            out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
+        if ls.a_scratch.numel() < need:
+            ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=store.device)
+        N.check(lib.pkv_attention_decode(ctypes_ref(st), nb, N.ptr(q), Hq, None, 0, N.ptr(out),
+                                         N.ptr(ls.a_scratch), int(ls.a_scratch.numel()), N.stream()),
+                "attention_decode")
+        return out
     if need > 0:
         stride = max(ls.tokens, nb * store.block + ls.nres_h, score_stride, 1)
         stride = (stride + 3) // 4 * 4
@@ -97,8 +114,11 @@ class _Captured:
         if self._out is None or self._out.shape != (B, Hq, D):
             self._out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
 
+    single_pass = True  # False: the three-launch path (also writes the score rows)
+
     def _attend(self, q: torch.Tensor) -> torch.Tensor:
-        return attention_decode_batched(self.store, self.layer, q, scores=self._scores, out=self._out)
+        return attention_decode_batched(self.store, self.layer, q, scores=self._scores, out=self._out,
+                                        single_pass=self.single_pass)
 
     def _graphable(self, q: torch.Tensor) -> bool:
         """Only the default format's folded-softmax launches (pkv_attention_decode)
@@ -245,6 +265,8 @@ class GraphedDecodeLoop:
     a caller that writes them in place and calls step() without arguments
     skips the copies."""
 
+    single_pass = True  # False: the three-launch attention path
+
     def __init__(self, store: CompressedStore, q_heads: int, layers=None, headroom: int = 16):
         self.store = store
         self.layers = list(range(store.layers)) if layers is None else list(layers)
@@ -311,7 +333,8 @@ class GraphedDecodeLoop:
                 N.check(lib.pkv_stage_token(L, N.ptr(self.k[i]), N.ptr(self.v[i]), N.stream()), "stage_token")
             N.check(lib.pkv_flush_staged(L, float(o.rel_scale_k), float(o.rel_scale_v), N.ptr(self._flush_scr[i]),
                                          int(self._flush_scr[i].numel()), N.stream()), "flush_staged")
-            attention_decode_batched(o, l, self.q[i], scores=self._scores[i], out=self.out[i], nblocks=self._cap[i])
+            attention_decode_batched(o, l, self.q[i], scores=self._scores[i], out=self.out[i], nblocks=self._cap[i],
+                                     single_pass=self.single_pass)
 
     def _capture(self):
         dev = torch.device(self.store.device)

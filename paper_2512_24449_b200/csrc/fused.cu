@@ -33,6 +33,10 @@ int64_t pkv_fast_v_scratch(const pkv_layer_t* L, int nblocks, int G);
 int64_t pkv_fast_attention_scratch(const pkv_layer_t* L, int nblocks, int G);
 int pkv_fast_attention(const pkv_layer_t* L, int nblocks, const float* q, int G, float* scores, int64_t sstride,
                        float* out, float* scratch, cudaStream_t s);
+// single-pass attention (attn_fused.cu)
+int64_t pkv_fast_attention1_scratch(const pkv_layer_t* L, int nblocks, int G);
+int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G, float* out, void* scratch,
+                        cudaStream_t s);
 
 namespace {
 
@@ -426,7 +430,8 @@ extern "C" int64_t pkv_attention_scratch_bytes(const pkv_layer_t* L, int32_t nbl
   int G = 0;
   if (fused_args(L, nblocks, q_heads, &G)) return -1;
   if (!pkv_fast_supported(L, G, 4)) return 0;
-  return pkv_fast_attention_scratch(L, nblocks, G);
+  const int64_t a3 = pkv_fast_attention_scratch(L, nblocks, G), a1 = pkv_fast_attention1_scratch(L, nblocks, G);
+  return a3 > a1 ? a3 : a1;
 }
 
 extern "C" int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const float* q, int32_t q_heads,
@@ -435,9 +440,18 @@ extern "C" int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const
   int G = 0;
   int s = fused_args(L, nblocks, q_heads, &G);
   if (s) return s;
-  if (!pkv_fast_supported(L, G, score_stride) || (reinterpret_cast<uintptr_t>(q) & 15)) {
+  if (!pkv_fast_supported(L, G, score_stride) || (reinterpret_cast<uintptr_t>(q) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15)) {
     pkv_set_error("attention_decode: only the default format (pack 16, head_dim 128, block 64, G <= 8) is fused");
     return PKV_E_ARG;
+  }
+  if (!scores) {  // single pass: no score rows
+    if (scratch_bytes < pkv_fast_attention1_scratch(L, nblocks, G) || (reinterpret_cast<uintptr_t>(scratch) & 15)) {
+      pkv_set_error("attention scratch too small or misaligned");
+      return PKV_E_ARG;
+    }
+    pkv_note_path(PKV_PATH_SINGLE);
+    return pkv_fast_attention1(L, nblocks, q, G, out, scratch, (cudaStream_t)stream);
   }
   if (score_stride < int64_t(nblocks) * L->block) {
     pkv_set_error("score_stride %lld < nblocks * block = %lld", (long long)score_stride,

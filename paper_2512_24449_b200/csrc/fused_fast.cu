@@ -43,539 +43,9 @@
 
 using namespace pkv;
 
+#include "fast_common.cuh"
+
 namespace {
-
-constexpr int kRows = 64, kD = 128, kP = 16;
-constexpr int kNib = 8, kMin = 8 + 256, kPar = kMin + 1024, kHdr = kPar + 256;  // 1544
-
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Wait for an mbarrier phase (the block normally is already there).
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// Bulk prefetch of global bytes into L2 (no shared memory, no barrier).
-__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_barrier_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// A fragment of m16n8k32 (rows = bytes of 16-byte smem rows, k = smem rows),
-// i.e. a byte transpose of 32 smem rows; lane L gives the address of row L.
-__device__ __forceinline__ void ldsm_t(uint32_t (&a)[4], uint32_t addr) {
-  asm volatile("ldmatrix.sync.aligned.m16n16.x2.trans.shared.b8 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
-               : "r"(addr));
-}
-// D = A(u8 16x32) * B(u8 32x8) + C
-__device__ __forceinline__ void imma_uu(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-// D = A(u8) * B(s8) + C
-__device__ __forceinline__ void imma_us(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ float h2f(uint32_t bits16) { return __half2float(__ushort_as_half(uint16_t(bits16))); }
-
-// a*b + c forced onto the FMA pipe (IMAD); the ALU pipe carries the selects.
-__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-__device__ __forceinline__ uint32_t umulhi(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
-__device__ __forceinline__ uint32_t shf_r_clamp(uint32_t lo, uint32_t hi, uint32_t s) {
-  uint32_t d;
-  asm("shf.r.clamp.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
-  return d;
-}
-__device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_t s) {
-  uint32_t d;
-  asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(s));
-  return d;
-}
-
-// Block reads.  Blocks staged in shared memory are addressed with 32-bit
-// shared-window addresses (LDS, no generic-address arithmetic); a block too
-// large to stage is read in place through a generic pointer.  The shared loads
-// are not volatile: their addresses derive from the slot offset read after the
-// slot's mbarrier wait, so they cannot be scheduled before it.
-__device__ __forceinline__ uint32_t ld32(const uint8_t* p) { return *(const uint32_t*)p; }
-__device__ __forceinline__ uint2 ld64(const uint8_t* p) { return *(const uint2*)p; }
-__device__ __forceinline__ uint4 ld128(const uint8_t* p) { return *(const uint4*)p; }
-__device__ __forceinline__ uint32_t ld32(uint32_t a) {
-  uint32_t v;
-  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint2 ld64(uint32_t a) {
-  uint2 v;
-  asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint4 ld128(uint32_t a) {
-  uint4 v;
-  asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ const uint8_t* gptr(const uint8_t* p) { return p; }
-__device__ __forceinline__ const uint8_t* gptr(uint32_t a) { return (const uint8_t*)__cvta_shared_to_generic(a); }
-
-// ---------------------------------------------------------------- unpack
-// Per-width constants (w <= 8; MA only for w <= 4): MA = 2^(16-4w), MB = 2^(32-2w), MC = 2^(8-w),
-// byte mask (2^w - 1) * 0x01010101.  Entry w at lut + 16*w.
-__device__ __forceinline__ void init_lut(uint4* lut, int tid) {
-  if (tid < 16) {
-    const uint32_t w = tid <= 8 ? tid : 8;
-    lut[tid] = make_uint4(w <= 4 ? 1u << (16 - 4 * w) : 0u, w ? 1u << (32 - 2 * w) : 0u, 1u << (8 - w),
-                          ((1u << w) - 1u) * 0x01010101u);
-  }
-}
-
-// (mask & a) | (~mask & b) in one LOP3 with the mask as its immediate
-template <uint32_t M>
-__device__ __forceinline__ uint32_t sel(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "n"(M), "r"(a), "r"(b));
-  return d;
-}
-
-// 8 fields of width w at stride w in x -> two registers of 4 bytes (fields
-// 0,1,4,5 and 2,3,6,7), masked to w bits, plus mr = min * 0x01010101.
-// Shifts are multiplies (FMA pipe), selects and masks are LOP3 (ALU pipe).
-__device__ __forceinline__ void spread8(uint32_t x, const uint4& c, uint32_t mr, uint32_t& ra, uint32_t& rb) {
-  const uint32_t t = sel<0x0000ffffu>(x, imad(x, c.x, 0u));  // fields 4..7 -> bit 16
-  const uint32_t tb = umulhi(t, c.y);                          // t >> 2w
-  const uint32_t ua = sel<0x00ff00ffu>(t, imad(t, c.z, 0u));
-  const uint32_t ub = sel<0x00ff00ffu>(tb, imad(tb, c.z, 0u));
-  ra = imad(ua & c.w, 1u, mr);
-  rb = imad(ub & c.w, 1u, mr);
-}
-
-#ifndef PKV_W2PRED
-#define PKV_W2PRED 0
-#endif
-#ifndef PKV_LUTREG
-#define PKV_LUTREG 0
-#endif
-#ifndef PKV_KREGC  // K kernel: width constants in registers (measured -3.5% time with the 5.9 KB ring)
-#define PKV_KREGC 1
-#endif
-// Shared-memory operands of one pack: the 3 words covering its <= 64-bit
-// payload (payload starts at bit `bit` of the block, bit % 16 == 0) and the
-// width's table entry.  Issued one pack ahead of the arithmetic.
-struct PackLd {
-  uint32_t w0, w1, w2;
-  uint4 c;
-};
-template <bool REGC = false, class P>
-__device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ lut, uint32_t bit, uint32_t w16) {
-  const P p = blk + ((bit >> 5) << 2);
-  PackLd r;
-  r.w0 = ld32(p);
-  r.w1 = ld32(p + 4);
-#if PKV_W2PRED
-  // the payload (16w bits from bit % 32 in {0, 16}) needs a third word only
-  // for w = 4 starting mid-word; other lanes skip the load (no bank traffic)
-  r.w2 = (w16 == 64u && (bit & 16u)) ? ld32(p + 8) : 0u;
-#else
-  // the payload (16w bits from bit % 32 in {0, 16}) reaches a third word only
-  // for w = 4 starting mid-word; loading it unconditionally (the ring keeps 16
-  // bytes of slack past every block) saves the predicate arithmetic, and the
-  // extra bits fall outside the 16 fields
-  r.w2 = ld32(p + 8);
-#endif
-  if (REGC || PKV_LUTREG) {
-    // the width constants from w in registers (7 ALU/FMA ops) instead of an
-    // LDS.128 per pack (4 wavefronts of the L1/shared data pipe, which runs at
-    // ~70% in the K kernel; the V kernel is closer to its ALU limit and keeps
-    // the table)
-    const uint32_t w = w16 >> 4;
-    const uint32_t mc = 0x100u >> w;                    // 2^(8-w)
-    const uint32_t mc2 = imad(mc, mc, 0u);              // 2^(16-2w)
-    const uint32_t ma = imad(mc2 >> 8, mc2 >> 8, 0u);   // 2^(16-4w)
-    r.c = make_uint4(ma, mc2 << 16, mc, (0x01010101u << w) - 0x01010101u);
-  } else {
-    r.c = *(const uint4*)(lut + w16);
-  }
-  return r;
-}
-// r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
-// 4 fields of width w <= 8 at stride w in x -> 4 bytes (fields 0..3), masked,
-// plus mr: the same two-level select tree as spread8 with the 8w-bit halves.
-__device__ __forceinline__ uint32_t spread4(uint32_t x, uint32_t a2, uint32_t c, uint32_t mask, uint32_t mr) {
-  const uint32_t t = sel<0x0000ffffu>(x, imad(x, a2, 0u));  // fields 2,3 -> bit 16
-  const uint32_t u = sel<0x00ff00ffu>(t, imad(t, c, 0u));   // fields 1,3 -> bits 8, 24
-  return imad(u & mask, 1u, mr);
-}
-// r[0..3] = the 16 codes at byte positions 0..15 (see tok()).  WIDE (blocks
-// holding any pack of width 5..8, a warp-uniform choice): such packs (80..128
-// payload bits over up to 5 words) take a second path; codes stay bytes
-// because the block check guarantees min + 2^w - 1 <= 255.  Blocks without
-// wide packs run the narrow code only.
-template <bool WIDE, class P>
-__device__ __forceinline__ void pack_decode(P blk, const PackLd& L, uint32_t bit, uint32_t w16, uint32_t mr,
-                                            uint32_t (&r)[4]) {
-  if (!WIDE || w16 <= 64u) {
-    const uint32_t x0 = shf_r_wrap(L.w0, L.w1, bit);  // payload bits 0..31
-    const uint32_t x1 = shf_r_wrap(L.w1, L.w2, bit);  // payload bits 32..63
-    const uint32_t md = imad(L.c.x, L.c.x, 0u);       // 2^(32-8w)
-    const uint32_t xh = imad(x1, md, umulhi(x0, md));  // fields 8..15 = payload >> 8w
-    spread8(x0, L.c, mr, r[0], r[1]);
-    spread8(xh, L.c, mr, r[2], r[3]);
-  } else {
-    const P p = blk + ((bit >> 5) << 2);
-    const uint32_t w3 = ld32(p + 12), w4 = ld32(p + 16);
-    const uint32_t w = w16 >> 4;
-    const uint32_t y0 = shf_r_wrap(L.w0, L.w1, bit), y1 = shf_r_wrap(L.w1, L.w2, bit);
-    const uint32_t y2 = shf_r_wrap(L.w2, w3, bit), y3 = shf_r_wrap(w3, w4, bit);
-    // fields 8..15 start at payload bit 8w (40..64)
-    const uint32_t s1 = 8u * w - 32u;
-    const uint32_t z0 = w == 8u ? y2 : shf_r_wrap(y1, y2, s1), z1 = w == 8u ? y3 : shf_r_wrap(y2, y3, s1);
-    const uint32_t a2 = imad(L.c.z, L.c.z, 0u);  // 2^(16-2w)
-    const uint32_t q0 = spread4(y0, a2, L.c.z, L.c.w, mr), q1 = spread4(shf_r_clamp(y0, y1, 4u * w), a2, L.c.z, L.c.w, mr);
-    const uint32_t q2 = spread4(z0, a2, L.c.z, L.c.w, mr), q3 = spread4(shf_r_clamp(z0, z1, 4u * w), a2, L.c.z, L.c.w, mr);
-    r[0] = __byte_perm(q0, q1, 0x5410u);  // fields 0, 1, 4, 5
-    r[1] = __byte_perm(q0, q1, 0x7632u);  // fields 2, 3, 6, 7
-    r[2] = __byte_perm(q2, q3, 0x5410u);
-    r[3] = __byte_perm(q2, q3, 0x7632u);
-  }
-}
-// width of pack i of a lane's 16 (nibbles nb), times 16
-__device__ __forceinline__ uint32_t w16_of(const uint2& nb, int i) {
-  const uint32_t nw = i < 8 ? nb.x : nb.y;
-  const int sh = 4 * (i & 7);
-  return (sh >= 4 ? (nw >> (sh - 4)) : (nw << 4)) & 0xf0u;
-}
-__device__ __forceinline__ uint32_t min_rep(const uint32_t (&mn)[8], int i) {
-  return __byte_perm(mn[i >> 1], 0u, (i & 1) ? 0x2222u : 0x0000u);
-}
-// byte position m within a pack's 16 bytes -> row within the row-group
-__host__ __device__ __forceinline__ int tok(int m) { return (m & 9) | ((m & 2) << 1) | ((m & 4) >> 1); }
-
-// Generic scalar field read (any width <= 15) for the slow path.
-__device__ __forceinline__ uint32_t field_at(const uint8_t* __restrict__ blk, uint32_t bitpos, uint32_t w) {
-  if (w == 0) return 0;
-  const uint8_t* p = blk + (bitpos >> 3);
-  const uint32_t sh = bitpos & 7;
-  const uint32_t v = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16);
-  return (v >> sh) & ((1u << w) - 1u);
-}
-__device__ __forceinline__ uint32_t pack_min(const uint8_t* __restrict__ blk, int p) {
-  return uint32_t(blk[kMin + 2 * p]) | (uint32_t(blk[kMin + 2 * p + 1]) << 8);
-}
-
-// ---------------------------------------------------------------- block parse
-// Lane `chunk` reads the width nibbles of physical packs 16*chunk .. +15 and the
-// 16 minima of chunk `mchunk` (its own, or the chunk it will decode).  Returns the lane's starting payload bit (warp scan over chunks in
-// lane order) and whether every pack of the block fits the fast path
-// (every code min + 2^w - 1 fits a byte, see below).
-struct Chunk {
-  uint2 nb;       // 16 width nibbles
-  uint32_t mn[8]; // 16 u16 minima
-  uint32_t bit;   // payload bit offset of the chunk's first pack
-  bool wide;      // the block has a pack of width 5..8 (warp-uniform)
-};
-// The parse in three steps so a caller can overlap it with independent work
-// (the V kernel's weight operand): loads, per-lane statistics, then one warp
-// vote (flag bits below, OR-reduced) and the 5-step scan.
-enum : uint32_t { kFWide = 1, kFGe8 = 2, kFMin240 = 4, kFMin128 = 8, kFNeg = 16 };
-template <class P>
-__device__ __forceinline__ void parse_load(P blk, int lane, int mchunk, Chunk& ch) {
-  ch.nb = ld64(blk + kNib + 8 * lane);
-  // minima of chunk `mchunk` (32 bytes at kMin + 32*mchunk = 264 + 32*mchunk):
-  // three aligned 16-byte loads from 256 + 32*mchunk, words 2..9
-  const uint4 m0 = ld128(blk + kMin - 8 + 32 * mchunk), m1 = ld128(blk + kMin + 8 + 32 * mchunk),
-              m2 = ld128(blk + kMin + 24 + 32 * mchunk);
-  ch.mn[0] = m0.z; ch.mn[1] = m0.w; ch.mn[2] = m1.x; ch.mn[3] = m1.y;
-  ch.mn[4] = m1.z; ch.mn[5] = m1.w; ch.mn[6] = m2.x; ch.mn[7] = m2.y;
-}
-// this lane's flag bits: a pack of width 5..8 (kFWide), of width >= 8 (kFGe8),
-// a minimum above 240 / 128.  The fast path needs every code min + 2^w - 1 to
-// fit a byte: w <= 4 everywhere and minima <= 240, or w <= 7 and minima <= 128
-// (w = 8 packs and larger minima take the scalar path).
-__device__ __forceinline__ uint32_t parse_flags(const Chunk& ch) {
-  uint32_t mor = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) mor |= ch.mn[q];
-  const uint32_t nx = ch.nb.x, ny = ch.nb.y;
-  const uint32_t ge8 = (nx | ny) & 0x88888888u;
-  const uint32_t ge5 = (((nx >> 2) & (nx | (nx >> 1))) & 0x11111111u) | (((ny >> 2) & (ny | (ny >> 1))) & 0x11111111u);
-  const uint32_t mo = (mor | (mor >> 16)) & 0xffffu;
-  return (ge5 ? kFWide : 0u) | (ge8 ? kFGe8 : 0u) | (mo > 240u ? kFMin240 : 0u) | (mo > 128u ? kFMin128 : 0u);
-}
-// warp-OR of the flags -> fast-path verdict and ch.wide
-__device__ __forceinline__ bool parse_verdict(uint32_t all, Chunk& ch) {
-  ch.wide = (all & kFWide) != 0;
-  return !(all & (kFGe8 | kFNeg | (ch.wide ? kFMin128 : kFMin240)));
-}
-// ch.bit = payload bit offset of chunk `lane` (warp scan over chunks in lane order)
-__device__ __forceinline__ void parse_scan(int lane, Chunk& ch) {
-  const uint32_t nx = ch.nb.x, ny = ch.nb.y;
-  uint32_t a = (nx & 0x0f0f0f0fu) + ((nx >> 4) & 0x0f0f0f0fu) + (ny & 0x0f0f0f0fu) + ((ny >> 4) & 0x0f0f0f0fu);
-  a = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu);
-  const uint32_t lsum = 16u * ((a & 0xffffu) + (a >> 16));  // payload bits (k = 16)
-  uint32_t inc = lsum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(PKV_FULL, inc, o);
-    if (lane >= o) inc += y;
-  }
-  ch.bit = 8u * kHdr + inc - lsum;
-}
-// Lane `chunk` reads the width nibbles of physical packs 16*chunk .. +15 and the
-// 16 minima of chunk `mchunk` (its own, or the chunk it will decode).  Returns
-// whether every pack of the block fits the fast path; ch.bit is the lane's
-// starting payload bit.
-template <class P>
-__device__ __forceinline__ bool parse_chunk(P blk, int lane, int mchunk, Chunk& ch) {
-  parse_load(blk, lane, mchunk, ch);
-  const bool fast = parse_verdict(__reduce_or_sync(PKV_FULL, parse_flags(ch)), ch);
-  parse_scan(lane, ch);
-  return fast;
-}
-
-// Slow-path descriptor table for any widths: desc[p] = payload bit (from the
-// block start, 18 bits) | width << 18.  Lane l covers packs 16l..16l+15.
-__device__ __forceinline__ void build_desc(const Chunk& ch, int lane, uint32_t* __restrict__ desc) {
-  uint32_t bit = ch.bit;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint32_t w = ((i < 8 ? ch.nb.x : ch.nb.y) >> (4 * (i & 7))) & 15u;
-    desc[16 * lane + i] = bit | (w << 18);
-    bit += 16u * w;
-  }
-  __syncwarp();
-}
-
-// ---------------------------------------------------------------- work split
-// The layer's blocks are numbered gb = u * NB + j (unit u = b * H + h, block j,
-// NB = blocks per sequence; sequences advance in lockstep).  Warp W of the
-// N = grid * warps-per-CTA warps owns the contiguous range [T*W/N, T*(W+1)/N)
-// of the T = U*NB blocks: every warp gets the same work to within one block
-// (no tail of idle SMs) and a range spans only a few units.  Warps are
-// independent: each streams its own blocks into its own shared-memory ring.
-struct Range {
-  int64_t b0, b1;
-};
-// With more warps than blocks (small layers: the grid is a whole number of
-// CTAs), warp W takes block W and the surplus warps come last: an empty range
-// in the middle of a unit would leave a partial-sum / score-maximum slot that
-// no warp writes (found by tests/test_gpu_parity.py::test_randomized_*).
-__host__ __device__ __forceinline__ Range warp_range(int64_t total, int64_t wid, int64_t nwarps) {
-  Range r;
-  if (nwarps > total) {
-    r.b0 = wid < total ? wid : total;
-    r.b1 = wid + 1 < total ? wid + 1 : total;
-  } else {
-    r.b0 = total * wid / nwarps;
-    r.b1 = total * (wid + 1) / nwarps;
-  }
-  return r;
-}
-// the warp whose range contains block gb
-__host__ __device__ __forceinline__ int64_t warp_of(int64_t gb, int64_t total, int64_t nwarps) {
-  return nwarps > total ? gb : ((gb + 1) * nwarps - 1) / total;
-}
-
-// Position (unit u = b * heads + h, block j) of a global block index,
-// advanced without division.
-struct Cursor {
-  int u, j, b, h;
-  __device__ __forceinline__ void init(int64_t gb, int NB, int heads) {
-    u = int(gb / NB);
-    j = int(gb - int64_t(u) * NB);
-    b = u / heads;
-    h = u - b * heads;
-  }
-  __device__ __forceinline__ void step(int by, int NB, int heads) {
-    j += by;
-    while (j >= NB) {
-      j -= NB;
-      ++u;
-      if (++h == heads) {
-        h = 0;
-        ++b;
-      }
-    }
-  }
-};
-
-// ---------------------------------------------------------------- per-warp feed
-// A warp streams its blocks with 1-D TMA bulk copies into a private byte ring
-// of RB bytes with NS mbarrier slots.  Bulk copies issued by one warp are
-// serviced one after another (~0.4 us each for 4 KB; tools/probe/
-// tma_feed_probe.cu), so every consumer warp is its own producer: a CTA-wide
-// producer warp caps the feed at ~1.4 TB/s per CTA.  Blocks are issued up to
-// NS - 1 ahead, as soon as the ring has room; a block's bytes stay valid until
-// the warp is done with it.
-#ifndef PKV_KPF  // L2 prefetch distance for the small-ring (K) feed, in blocks
-#define PKV_KPF 2  // measured -1.5% on K (5.9 KB ring holds ~1 block); 0 for the V ring
-#endif
-#ifndef PKV_VPF  // the same for the V feed (11 KB ring)
-#define PKV_VPF 0
-#endif
-template <int RB, int NS>
-struct Feed {
-  uint8_t* ring;
-  uint64_t* bar;     // [NS] full barriers (count 1 + tx bytes)
-  uint32_t* pos;     // [NS] ring offset of the block in the slot
-  uint32_t* abs;     // [NS] absolute start (for space accounting)
-  const uint8_t** gsrc;  // [NS] non-null: block larger than the ring, read in place from global memory
-  int* present;      // [NS] 1: the slot holds a block (0: past the sequence's nblk)
-  uint32_t head;     // absolute allocation point
-  int issued;        // blocks issued so far
-  // directory of the warp's blocks, lane-distributed: entry k0 + lane
-  int k0;
-  int64_t offl;
-  int lenl;          // -1: no block (past nblk)
-
-  __device__ __forceinline__ void init(uint8_t* smem, int lane) {
-    ring = smem;
-    bar = (uint64_t*)(smem + RB);
-    gsrc = (const uint8_t**)(bar + NS);
-    pos = (uint32_t*)(gsrc + NS);
-    abs = pos + NS;
-    present = (int*)(abs + NS);
-    head = 0;
-    issued = 0;
-    k0 = -32;
-    if (lane == 0) {
-      for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
-      fence_barrier_init();
-    }
-    __syncwarp();
-  }
-  static constexpr size_t bytes() { return RB + NS * 28; }
-
-  // (re)load the directory entries of the warp's blocks kk .. kk+31
-  __device__ __forceinline__ void load_dir(const pkv_layer_t& L, int kind, int NB, const Range& rg, int kk, int lane) {
-    k0 = kk;
-    const int64_t gb = rg.b0 + kk + lane;
-    offl = 0;
-    lenl = -1;
-    if (gb < rg.b1) {
-      const int u = int(gb / NB), j = int(gb - int64_t(u) * NB);
-      if (j < L.nblk[u / L.heads]) {
-        const int64_t tab = (int64_t(kind) * L.batch * L.heads + u) * L.max_blocks + j;
-        offl = L.blk_off[tab];
-        lenl = L.blk_len[tab];
-      }
-    }
-  }
-  // issue the warp's next block if the ring has room; false when it has not
-  __device__ __forceinline__ bool try_issue(const pkv_layer_t& L, int kind, int NB, const Range& rg, int nk,
-                                            uint32_t tail, int lane) {
-    if (issued >= nk) return false;
-    if (issued >= k0 + 32) load_dir(L, kind, NB, rg, issued, lane);
-    const int len = __shfl_sync(PKV_FULL, lenl, issued - k0);
-    const int64_t off = __shfl_sync(PKV_FULL, offl, issued - k0);
-    const bool big = len + 16 + 16 > RB;              // cannot be staged: read in place
-    const uint32_t bytes = (len < 0 || big) ? 0u : uint32_t((len + 15) & ~15);
-    const uint32_t size = (len < 0 || big) ? 0u : bytes + 16;  // +16: slack for the decoders' word over-reads
-    uint32_t p = head % RB, skip = 0;
-    if (p + size > RB) {
-      skip = RB - p;
-      p = 0;
-    }
-    // the skipped tail bytes are never live: with nothing in flight the block
-    // can always start at offset 0
-    const uint32_t live = tail == head ? head + skip : tail;
-    if (head + skip + size - live > RB) return false;
-    const int s = issued % NS;
-    if (lane == 0) {
-      pos[s] = p;
-      abs[s] = head + skip;
-      gsrc[s] = big ? L.arena + off : nullptr;
-      present[s] = len >= 0;
-      if (len < 0 || big) {
-        mbar_arrive(&bar[s]);
-      } else {
-        // the ring bytes being overwritten were last read through the generic proxy
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], bytes);
-        tma_load_1d(ring + p, L.arena + off, bytes, &bar[s]);
-      }
-    }
-    __syncwarp();
-    head += skip + size;
-    ++issued;
-    prefetch_ahead<(RB < 8192 ? PKV_KPF : PKV_VPF)>(L, nk, lane);
-    return true;
-  }
-  // L2 prefetch of the block PF positions past the newest issued one (PF = 0: off)
-  template <int PF>
-  __device__ __forceinline__ void prefetch_ahead(const pkv_layer_t& L, int nk, int lane) {
-    const int t = issued - 1 + PF;
-    if (PF > 0 && t < nk && t >= k0 && t - k0 < 32) {
-      const int len = __shfl_sync(PKV_FULL, lenl, t - k0);
-      const int64_t off = __shfl_sync(PKV_FULL, offl, t - k0);
-      if (lane == 0 && len > 0) l2_prefetch(L.arena + off, uint32_t((len + 15) & ~15));
-    }
-  }
-  // oldest ring byte still needed once block k is finished
-  __device__ __forceinline__ uint32_t tail_after(int k) const { return k + 1 < issued ? abs[(k + 1) % NS] : head; }
-  // top up: issue while there is room and a free slot (at most NS - 1 ahead of k)
-  __device__ __forceinline__ void refill(const pkv_layer_t& L, int kind, int NB, const Range& rg, int nk, int k,
-                                         uint32_t tail, int lane) {
-    while (issued < nk && issued < k + NS && try_issue(L, kind, NB, rg, nk, tail, lane)) {
-    }
-  }
-  // wait for block k; returns its bytes in the ring, or sets *g to the block
-  // in global memory when it was too large to stage (then the ring pointer is
-  // meaningless)
-  // (*have = the block exists: a sequence shorter than the grid's block count
-  // has no block there.  Read from shared memory, so the test never waits on a
-  // global-load scoreboard shared with loads just issued, e.g. the next
-  // block's weights: ~16% of the V kernel's time stalled there with nblk[b]
-  // read from global memory.)
-  __device__ __forceinline__ uint32_t wait(int k, const uint8_t** g, bool* have) {
-    const int s = k % NS;
-    mbar_wait(&bar[s], uint32_t((k / NS) & 1));
-    *g = gsrc[s];
-    *have = present[s] != 0;
-    return smem_u32(ring) + pos[s];
-  }
-};
 
 // ======================================================================= K
 // Per-warp tile: [row-group g][channel c][16 bytes], row R = 128g + c at byte
@@ -618,92 +88,6 @@ constexpr int kRBK = PKV_RBK, kNSK = PKV_NSK;
 using FeedK = Feed<kRBK, kNSK>;
 constexpr size_t kWarpSmemK = (kTile + FeedK::bytes() + 127) / 128 * 128;
 
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(PKV_FULL, v, o));
-  return v;
-}
-__device__ __forceinline__ float sel8(const float (&v)[8], int i) {
-  float r = v[0];
-#pragma unroll
-  for (int k = 1; k < 8; ++k) r = i == k ? v[k] : r;
-  return r;
-}
-
-// Query operand of one unit for this lane (B fragments of the IMMA): k-step jj
-// covers channels 32jj..32jj+31, b0 = channels 32jj + 4tq + e, b1 = +16.
-// Column gi of unsigned tile nu = (head 4nu + gi/2, byte digit gi&1) of
-// x = rint(q * f_head) (|x| <= 2^22, f_head a power of two); signed tile S
-// column 2t = (head t, digit 2), 2t+1 = (head t+4, digit 2) or zero.
-template <int NU>
-struct QFrag {
-  uint32_t u[NU][4][2], s[4][2];
-  float qs[2], inv[2];  // sum(q) and 1/f of heads tq and tq+4
-};
-template <int NU>
-__device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G, int lane, QFrag<NU>& F) {
-  const int gi = lane >> 2, tq = lane & 3;
-  constexpr int GH = 4 * NU;  // heads covered by the fragments (4 or 8)
-  float mx[8], sm[8];
-#pragma unroll
-  for (int g = 0; g < 8; ++g) mx[g] = sm[g] = 0.f;
-#pragma unroll
-  for (int g = 0; g < GH; ++g) {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (g < G) v = *(const float4*)(qu + g * kD + 4 * lane);
-    mx[g] = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-    sm[g] = (v.x + v.y) + (v.z + v.w);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int g = 0; g < GH; ++g) {
-      mx[g] = fmaxf(mx[g], __shfl_xor_sync(PKV_FULL, mx[g], o));
-      sm[g] += __shfl_xor_sync(PKV_FULL, sm[g], o);
-    }
-  float f[8];
-#pragma unroll
-  for (int g = 0; g < 8; ++g) {
-    const int eb = (__float_as_int(mx[g]) >> 23) & 0xff;
-    // f = 2^(21 - e) for max in [2^e, 2^(e+1)): |q * f| < 2^22
-    f[g] = __int_as_float(max(1, min(275 - eb, 254)) << 23);
-  }
-  F.qs[0] = sel8(sm, tq);
-  F.qs[1] = sel8(sm, tq + 4);
-  F.inv[0] = 1.f / sel8(f, tq);
-  F.inv[1] = 1.f / sel8(f, tq + 4);
-  // x = rint(q*f) via the 1.5*2^23 magic: bits - 0x4B400000 = x for |x| < 2^22;
-// digits: byte 0, byte 1 (unsigned) and byte 2 (signed: x >> 16)
-  auto digits = [&](int g, int jj, int r, uint32_t (&x)[4]) {
-    const float4 v = *(const float4*)(qu + g * kD + 32 * jj + 16 * r + 4 * tq);
-    const float fg = sel8(f, g);
-    x[0] = __float_as_uint(fmaf(v.x, fg, 12582912.f)) - 0x4B400000u;
-    x[1] = __float_as_uint(fmaf(v.y, fg, 12582912.f)) - 0x4B400000u;
-    x[2] = __float_as_uint(fmaf(v.z, fg, 12582912.f)) - 0x4B400000u;
-    x[3] = __float_as_uint(fmaf(v.w, fg, 12582912.f)) - 0x4B400000u;
-  };
-  const int gsS = (gi >> 1) + 4 * (gi & 1);
-  const bool useS = ((gi & 1) == 0 || NU == 2) && gsS < G;
-#pragma unroll
-  for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-#pragma unroll
-      for (int nu = 0; nu < NU; ++nu) {
-        const int g = 4 * nu + (gi >> 1);
-        uint32_t x[4] = {0u, 0u, 0u, 0u};
-        if (g < G) digits(g, jj, r, x);
-        const uint32_t lo = __byte_perm(x[0], x[1], (gi & 1) ? 0x0051u : 0x0040u);
-        const uint32_t hi = __byte_perm(x[2], x[3], (gi & 1) ? 0x0051u : 0x0040u);
-        F.u[nu][jj][r] = __byte_perm(lo, hi, 0x5410u);
-      }
-      uint32_t x[4] = {0u, 0u, 0u, 0u};
-      if (useS) digits(gsS, jj, r, x);
-      const uint32_t lo = __byte_perm(x[0], x[1], 0x0062u);
-      const uint32_t hi = __byte_perm(x[2], x[3], 0x0062u);
-      F.s[jj][r] = __byte_perm(lo, hi, 0x5410u);
-    }
-}
 
 
 // ST: also record softmax statistics for attention_decode: the maximum score of

@@ -1,0 +1,167 @@
+"""Parity of the single-pass decode attention (attn_fused_kernel, §8 f1).
+
+attention_decode as ONE launch: K decode, online softmax
+and V decode block by block, per-warp partials merged in a fixed order.
+Checked against the f64 oracle -- softmax(naive_k_scores / sqrt(d)) fed to
+naive_v_output over the oracle's own compressed store (oracle/
+packkv_oracle.py) -- with tolerance ||gpu - f64||_inf <= 1e-3 * ||f64||_inf
+(SURVEY Appendix A #12), for G in {1..8}, residues straddling the 32-row
+residue chunks, wide packs (scalar paths, blocks read in place), the
+BASELINE config shapes on sampled sequences, and against the three-launch
+path.  Every call asserts pkv_last_path() == PATH_SINGLE."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import packkv_oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+def _mods():
+    from paper_2512_24449_b200 import _native as N
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    from paper_2512_24449_b200.kv_store import CompressedStore
+    return N, attention_decode_batched, CompressedStore
+
+
+def _close(a, ref):
+    a = np.asarray(a, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = max(np.abs(ref).max(), 1e-30)
+    err = np.abs(a - ref).max()
+    assert err <= TOL * scale, f"max abs err {err:.3e} > {TOL} * {scale:.3e}"
+    return err / scale
+
+
+def _oracle_attention(ref, h, q):
+    s = O.naive_k_scores(ref, 0, h, q).astype(np.float64) / math.sqrt(ref.head_dim)
+    return O.naive_v_output(ref, 0, h, O.softmax64(s))
+
+
+def _single(N, A, st, q, **kw):
+    out = A(st, 0, q, **kw)
+    assert N.last_path() == N.PATH_SINGLE, "attention left the single-pass kernel"
+    return out
+
+
+@pytest.mark.parametrize("rels", [(0.1, 0.2), (0.02, 0.03)], ids=["paper_rel", "wide_packs"])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 5, 8])
+def test_single_pass_vs_oracle(G, rels):
+    N, A, CS = _mods()
+    rng = np.random.default_rng(500 + G)
+    B, H, D = 2, 2, 128
+    for T in (64 * 9 + 45, 64 * 3, 31, 64 * 4 + 1):
+        k = O.gen_gauss_outlier(rng, B * H * T, D, 4).reshape(B, H, T, D).transpose(0, 2, 1, 3).copy()
+        v = O.gen_gauss_outlier(rng, B * H * T, D, 1).reshape(B, H, T, D).transpose(0, 2, 1, 3).copy()
+        st = CS(1, H, D, batch=B, rel_scale_k=rels[0], rel_scale_v=rels[1])
+        st.compress_batch(0, k, v)
+        q = (rng.standard_normal((B, H * G, D)) * 3).astype(np.float32)
+        out = _single(N, A, st, torch.from_numpy(q)).cpu().numpy()
+        for b in range(B):
+            ref = O.OracleStore(1, H, D, rel_k=rels[0], rel_v=rels[1])
+            ref.compress_batch(0, k[b], v[b])
+            for hq in range(H * G):
+                _close(out[b, hq], _oracle_attention(ref, hq // G, q[b, hq]))
+
+
+# (name, batch, kv heads, G, tokens, sampled sequences)
+CONFIG_SHAPES = [
+    ("B", 8, 8, 4, 8192, (0, 7)),
+    ("E", 2, 8, 8, 16384, (1,)),
+    ("D", 1, 52, 1, 2048, (0,)),
+    ("C", 1, 40, 1, 2048, (0,)),
+]
+
+
+@pytest.mark.parametrize("r", [0, 33])
+@pytest.mark.parametrize("cfg", CONFIG_SHAPES, ids=[c[0] for c in CONFIG_SHAPES])
+def test_single_pass_config_shapes_vs_oracle(cfg, r):
+    from paper_2512_24449_b200.tensor_model import gauss_outlier
+    name, B, H, G, T0, samples = cfg
+    N, A, CS = _mods()
+    T = T0 + r
+    k = gauss_outlier((B, T, H, 128), seed=3 + r)
+    v = gauss_outlier((B, T, H, 128), n_outlier=1, seed=10 + r)
+    st = CS(1, H, 128, batch=B, max_tokens=T)
+    st.compress_batch(0, k, v)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(r)
+    q = torch.randn((B, H * G, 128), device="cuda", generator=g) * 2
+    out = _single(N, A, st, q).cpu().numpy()
+    qh = q.cpu().numpy()
+    for b in samples:
+        ref = O.OracleStore(1, H, 128)
+        ref.compress_batch(0, k[b].cpu().numpy(), v[b].cpu().numpy())
+        heads = range(H) if H <= 8 else (0, 17, H - 1)
+        for h in heads:
+            for hq in (h * G, h * G + G - 1):
+                _close(out[b, hq], _oracle_attention(ref, h, qh[b, hq]))
+
+
+def test_single_pass_matches_three_launch_and_is_deterministic():
+    """The single pass agrees with the three-launch path (scores written)
+    within f32 accumulation (1e-5 relative) and is bit-identical run to run
+    and across block-count headroom (nblocks larger than the store)."""
+    N, A, CS = _mods()
+    rng = np.random.default_rng(9)
+    B, H, G, D, T = 3, 4, 4, 128, 64 * 50 + 17
+    k = rng.standard_normal((B, T, H, D)).astype(np.float16)
+    v = rng.standard_normal((B, T, H, D)).astype(np.float16)
+    st = CS(1, H, D, batch=B)
+    st.compress_batch(0, k, v)
+    q = torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32) * 2).cuda()
+    one = _single(N, A, st, q).clone()
+    two = _single(N, A, st, q).clone()
+    assert torch.equal(one, two)
+    three = A(st, 0, q, single_pass=False)
+    assert N.last_path() == N.PATH_FAST
+    assert float((one - three).abs().max() / three.abs().max()) <= 1e-5
+    st[0]._ensure(8)
+    hr = _single(N, A, st, q, nblocks=st[0].nblk_h + 8)
+    assert float((hr - three).abs().max() / three.abs().max()) <= 1e-5
+
+
+def test_single_pass_softmax_edges():
+    """One-token cache -> the V row (softmax of a singleton);
+    identical K rows (uniform weights over the compressed rows); very large
+    score spreads (one row dominates)."""
+    N, A, CS = _mods()
+    D = 128
+    rng = np.random.default_rng(4)
+    st = CS(1, 1, D)
+    kv = rng.standard_normal((1, 1, D)).astype(np.float16)
+    vv = rng.standard_normal((1, 1, D)).astype(np.float16)
+    st.compress_batch(0, kv, vv)
+    out = _single(N, A, st, torch.from_numpy(rng.standard_normal((1, 1, D)).astype(np.float32))).cpu().numpy()
+    np.testing.assert_allclose(out[0, 0], vv[0, 0].astype(np.float32), rtol=1e-6, atol=1e-6)
+    T = 64 * 6 + 5
+    st = CS(1, 1, D)
+    krow = rng.standard_normal(D).astype(np.float16)
+    vv = rng.standard_normal((T, 1, D)).astype(np.float16)
+    st.compress_batch(0, np.broadcast_to(krow, (T, 1, D)).copy(), vv)
+    q = rng.standard_normal(D).astype(np.float32)
+    out = _single(N, A, st, torch.from_numpy(q[None, None])).cpu().numpy()
+    ref = O.OracleStore(1, 1, D)
+    ref.compress_batch(0, np.broadcast_to(krow, (T, 1, D)).copy(), vv)
+    # the compressed rows dequantize identically (the staged residue rows stay fp16)
+    _close(out[0, 0], _oracle_attention(ref, 0, q))
+    nb = 64 * (T // 64)
+    s = O.naive_k_scores(ref, 0, 0, q)
+    assert np.all(s[:nb] == s[0])
+    # a score spread of ~1e3: exp underflows for almost every row
+    T = 64 * 20 + 7
+    kk = rng.standard_normal((T, 1, D)).astype(np.float16)
+    vv = rng.standard_normal((T, 1, D)).astype(np.float16)
+    st = CS(1, 1, D)
+    st.compress_batch(0, kk, vv)
+    ref = O.OracleStore(1, 1, D)
+    ref.compress_batch(0, kk, vv)
+    q = (rng.standard_normal(D) * 60).astype(np.float32)
+    out = _single(N, A, st, torch.from_numpy(q[None, None])).cpu().numpy()
+    _close(out[0, 0], _oracle_attention(ref, 0, q))
