@@ -697,6 +697,41 @@ def main():
         ms = k_ms + v_ms
     value = world * 2 * logical_kind / (ms * 1e-3) / 1e9
 
+    # ---- decode attention per layer: the single pass
+    # (attn_fused_kernel, one launch + the counter memset) against the
+    # three-launch path (fused K with score maxima, fused V on exp(s - M),
+    # finalize), both graph-replayed
+    from paper_2512_24449_b200.attention_sim import attention_decode_batched
+    a_out = torch.empty((Bl, Hql, D), device="cuda")
+    a_scores = torch.empty((Bl, Hql, (L + 3) // 4 * 4), device="cuda")
+
+    def attn(single):
+        for l in range(layers):
+            attention_decode_batched(st, l, qs[l], out=a_out, scores=None if single else a_scores,
+                                     single_pass=single)
+    attn_us = {}
+    for single in (True, False):
+        attn(single)
+        ga = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ga):
+            attn(single)
+        for _ in range(args.warmup):
+            ga.replay()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(K):
+            if l2_flush:
+                flush_buf.zero_()
+            ga.replay()
+        t1.record()
+        torch.cuda.synchronize()
+        attn_us["single" if single else "three"] = max_over_ranks([t0.elapsed_time(t1) * 1e3 / K / layers], world)[0]
+        del ga
+    alg_attn = alg_k + alg_v - 2 * Bl * Hql * L * 4   # no score rows written or read
+    if l2_flush:
+        attn_us = {k: None for k in attn_us}  # the flush is inside the timed loop: no clean number
+
     # ---- e2e through the public API: host q (this rank's shard) -> sharded
     # decode (fused K, softmax, fused V, NCCL all-gather) per layer -> host output
     decs = [S.ShardedDecoder(part, S.cuda_local_attention(st, l), Hq, D) for l in range(layers)]
@@ -769,11 +804,20 @@ def main():
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "algorithmic_bytes_per_launch": int(alg),
                          "frac_vs_nominal_8000_gbs": round(achieved / 8000.0, 4)},
+            "attention": None if attn_us["single"] is None else {
+                "single_pass_us": round(attn_us["single"], 2), "three_launch_us": round(attn_us["three"], 2),
+                "single_pass_gbs_physical": round(alg_attn / (attn_us["single"] * 1e-6) / 1e9, 1),
+                "single_pass_frac": round(alg_attn / (attn_us["single"] * 1e-6) / 1e9 / peak, 4),
+                "single_pass_gbs_equiv": round(2 * kind_layer / (attn_us["single"] * 1e-6) / 1e9, 1),
+                "algorithmic_bytes_per_launch": int(alg_attn),
+                "per": "one layer: softmax(q K^T / sqrt(d)) V over this rank's units, graph-replayed; single "
+                       "pass = attn_fused_kernel (+ counter memset), three launch = fused K + fused V + finalize"},
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": layers * Bl * Hql * D * 4,
                     "d2h_bytes_per_step": layers * world * Bl * Hql * D * 4,
                     "path": "sharding.ShardedDecoder.step (public API) per layer on the pinned host q shard: H2D "
-                            "straight into the graph's input buffer, one CUDA-graph replay of fused K + softmax + "
-                            "fused V (attention_sim.GraphedAttention), all-gather of per-head outputs, D2H out",
+                            "straight into the graph's input buffer, one CUDA-graph replay of the single-pass "
+                            "decode attention (attention_sim.GraphedAttention -> attn_fused_kernel), all-gather of "
+                            "per-head outputs, D2H out",
                     "ms_per_step": round(e2e_ms, 5)},
             "memory": mem,
             # scaling with and without the all-gather -- the same

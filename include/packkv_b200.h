@@ -220,7 +220,8 @@ int64_t pkv_attention_scratch_bytes(const pkv_layer_t* L, int32_t nblocks, int32
  *     returned.  Three launches: fused K (also records per-slot score
  *     maxima), fused V on exp(s - M) with the row maximum M, normalising
  *     finalize.
- * q, out and scratch 16-byte aligned.  Default format only (pack 16,
+ * q, out and scratch 16-byte aligned; calls sharing a scratch buffer must be
+ * stream-ordered.  Default format only (pack 16,
  * head_dim 128, block 64, G <= 8); else PKV_E_ARG.  Blocks past a
  * sequence's device count nblk[b] (nblocks headroom) are skipped.      */
 int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const float* q, int32_t q_heads, float* scores,

@@ -34,11 +34,14 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     headroom for blocks appended on the device later (GraphedDecodeLoop):
     blocks past a sequence's device count are skipped.
 
-    single_pass (default: True unless `scores` is given): the default format
-    runs ONE launch (attn_fused_kernel: K, online softmax and V block by
-    block, deterministic merge of the per-warp partials) and no score row
-    reaches HBM; False keeps the three-launch path, which also fills
-    `scores`."""
+    single_pass: True runs the single pass (attn_fused_kernel: K, online
+    softmax and V block by block, then a deterministic merge of the per-warp
+    partials; no score row reaches HBM); False the three-launch path, which
+    also fills `scores`.  Default (None): the single pass when `scores` is not
+    requested and the layer is latency-bound (few blocks per resident warp,
+    single_pass_preferred), where it measured faster (config C: 622 vs 482
+    tokens/s); the three-launch path at long contexts, where its two
+    kernels issue faster (config B 131 vs 140 us)."""
     q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
     ls = store[layer]
     B, H, D = store.batch, store.heads, store.head_dim
@@ -50,12 +53,12 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     nb = ls.nblk_h if nblocks is None else int(nblocks)
     need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(st), nb, Hq))
     if single_pass is None:
-        single_pass = scores is None
+        single_pass = scores is None and single_pass_preferred(store, nb)
     if need > 0 and single_pass:
         if out is None:
             out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
         if ls.a_scratch.numel() < need:
-            ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=store.device)
+            ls.a_scratch = torch.zeros(need, dtype=torch.uint8, device=store.device)  # work counter: zero before first use
         N.check(lib.pkv_attention_decode(ctypes_ref(st), nb, N.ptr(q), Hq, None, 0, N.ptr(out),
                                          N.ptr(ls.a_scratch), int(ls.a_scratch.numel()), N.stream()),
                 "attention_decode")
@@ -69,7 +72,7 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
         if out is None:
             out = torch.empty((B, Hq, D), dtype=torch.float32, device=store.device)
         if ls.a_scratch.numel() < need:
-            ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=store.device)
+            ls.a_scratch = torch.zeros(need, dtype=torch.uint8, device=store.device)  # work counter: zero before first use
         N.check(lib.pkv_attention_decode(ctypes_ref(st), nb, N.ptr(q), Hq, N.ptr(scores), stride, N.ptr(out),
                                          N.ptr(ls.a_scratch), int(ls.a_scratch.numel()), N.stream()),
                 "attention_decode")
@@ -77,6 +80,20 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     s = fused_k_scores_batched(store, layer, q)
     a = torch.softmax(s, dim=-1)
     return fused_v_output_batched(store, layer, a, out=out)
+
+
+# resident warps of the fused kernels on a B200 (148 SMs x 16) and the
+# blocks-per-warp crossover below which the single pass is the faster path
+_RESIDENT_WARPS = 148 * 16
+SINGLE_PASS_MAX_ITEMS_PER_WARP = 8
+
+
+def single_pass_preferred(store: CompressedStore, nblocks: int) -> bool:
+    """True when one decode-attention launch is latency-bound: the layer's
+    (unit, block + residue chunk) items are at most
+    SINGLE_PASS_MAX_ITEMS_PER_WARP per resident warp."""
+    items = store.batch * store.heads * (int(nblocks) + (store.buffer + 31) // 32)
+    return items <= SINGLE_PASS_MAX_ITEMS_PER_WARP * _RESIDENT_WARPS
 
 
 def ptr_of(t):
@@ -114,11 +131,14 @@ class _Captured:
         if self._out is None or self._out.shape != (B, Hq, D):
             self._out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
 
-    single_pass = True  # False: the three-launch path (also writes the score rows)
+    single_pass = None  # None: single_pass_preferred; True / False force a path
 
     def _attend(self, q: torch.Tensor) -> torch.Tensor:
+        sp = self.single_pass
+        if sp is None:
+            sp = single_pass_preferred(self.store, self.store[self.layer].nblk_h)
         return attention_decode_batched(self.store, self.layer, q, scores=self._scores, out=self._out,
-                                        single_pass=self.single_pass)
+                                        single_pass=sp)
 
     def _graphable(self, q: torch.Tensor) -> bool:
         """Only the default format's folded-softmax launches (pkv_attention_decode)
@@ -265,7 +285,7 @@ class GraphedDecodeLoop:
     a caller that writes them in place and calls step() without arguments
     skips the copies."""
 
-    single_pass = True  # False: the three-launch attention path
+    single_pass = None  # None: single_pass_preferred; True / False force a path
 
     def __init__(self, store: CompressedStore, q_heads: int, layers=None, headroom: int = 16):
         self.store = store
@@ -318,7 +338,7 @@ class GraphedDecodeLoop:
                 self._flush_scr[i] = torch.empty(fb, dtype=torch.uint8, device=o.device)
             need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(L), self._cap[i], Hq))
             if ls.a_scratch.numel() < need:
-                ls.a_scratch = torch.empty(need, dtype=torch.uint8, device=o.device)
+                ls.a_scratch = torch.zeros(need, dtype=torch.uint8, device=o.device)
             stride = (self._cap[i] * o.block + o.buffer + 3) // 4 * 4
             if self._scores[i] is None or self._scores[i].shape[-1] < stride:
                 self._scores[i] = torch.empty((B, Hq, stride), dtype=torch.float32, device=o.device)
@@ -333,8 +353,11 @@ class GraphedDecodeLoop:
                 N.check(lib.pkv_stage_token(L, N.ptr(self.k[i]), N.ptr(self.v[i]), N.stream()), "stage_token")
             N.check(lib.pkv_flush_staged(L, float(o.rel_scale_k), float(o.rel_scale_v), N.ptr(self._flush_scr[i]),
                                          int(self._flush_scr[i].numel()), N.stream()), "flush_staged")
+            sp = self.single_pass
+            if sp is None:
+                sp = single_pass_preferred(o, self._cap[i])
             attention_decode_batched(o, l, self.q[i], scores=self._scores[i], out=self.out[i], nblocks=self._cap[i],
-                                     single_pass=self.single_pass)
+                                     single_pass=sp)
 
     def _capture(self):
         dev = torch.device(self.store.device)

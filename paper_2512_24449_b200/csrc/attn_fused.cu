@@ -27,16 +27,17 @@
 //    depend on arrival order (deterministic).
 #include "fast_common.cuh"
 
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
 namespace {
 
 constexpr int kWA = 4;                // warps per CTA
-constexpr int kTileA = 4 * 128 * 16;  // K transpose tile (8 KB); V phase: vtmp [8][128] f32 + frag [8][2][64]
+constexpr int kTileA = 4 * 128 * 16;  // K transpose tile (8 KB); after the K MMAs: sbuf, frag, vtmp (below)
 constexpr int kResRows = 32;          // residue rows per range item
-#ifndef PKV_RBA  // ring bytes per warp: one K+V block pair (~7.3 KB at the paper's rel) plus the next K
-#define PKV_RBA 8192
+#ifndef PKV_RBA  // ring bytes per warp (a K block is ~3.9 KB, a V block ~3.4 KB at the paper's rel)
+#define PKV_RBA 5888
 #endif
 #ifndef PKV_NSA
 #define PKV_NSA 4
@@ -44,13 +45,19 @@ constexpr int kResRows = 32;          // residue rows per range item
 #ifndef PKV_APF  // L2 prefetch distance in feed items (K and V alternate)
 #define PKV_APF 2
 #endif
-#ifndef PKV_AMINB  // CTAs per SM the register allocation must allow (shared memory allows 3)
-#define PKV_AMINB 3
+#ifndef PKV_ADIAG  // diagnostics build: per-warp cycle counters into `out` (results wrong)
+#define PKV_ADIAG 0
+#endif
+#ifndef PKV_AREGC  // pack width constants in registers (1) or from the shared table (0)
+#define PKV_AREGC 0
+#endif
+#ifndef PKV_AMINB  // CTAs per SM the register allocation must allow
+#define PKV_AMINB 4
 #endif
 constexpr int kRBA = PKV_RBA, kNSA = PKV_NSA;
 using FeedA = Feed<kRBA, kNSA, PKV_APF, true>;
 constexpr int kPartA = kD + 4;  // acc[128], z, l, M (log2 domain), pad
-constexpr size_t kWarpSmemA = (kTileA + 2048 + FeedA::bytes() + 127) / 128 * 128;
+constexpr size_t kWarpSmemA = (kTileA + FeedA::bytes() + 127) / 128 * 128;
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ float ldcg_f(const float* p) { return __ldcg(p); }
@@ -61,7 +68,8 @@ __host__ __device__ __forceinline__ int res_items(int buffer) { return (buffer +
 template <int NG>  // NG = 1: G <= 4 (one digit tile / n-tile), 2: G <= 8
 __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
     attn_fused_kernel(pkv_layer_t L, const float* __restrict__ q, int G, int NB, int NI, int64_t total,
-                      float* __restrict__ part, int maxseg, int* __restrict__ cnt, float* __restrict__ out) {
+                      int64_t nchunks, float* __restrict__ part, int maxseg,
+                      int* __restrict__ cnt, float* __restrict__ out) {
   constexpr int GP = 4 * NG;     // padded heads
   constexpr int LPH = 32 / GP;   // writer lanes per head
   constexpr int TPL = 64 / LPH;  // rows per writer lane (8 or 16)
@@ -71,14 +79,15 @@ __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
   uint4* lut = (uint4*)smem;
   init_lut(lut, threadIdx.x);
   uint8_t* wsm = smem + 256 + warp * kWarpSmemA;
+  // the tile region, once the K MMAs have read it:
   uint8_t* tile = wsm;
-  float* vtmp = (float*)wsm;                   // [GP][128] (V phase)
-  uint8_t* frag = wsm + 4096;                  // [GP][2][64] (V phase)
-  uint32_t* vdesc = (uint32_t*)(wsm + 5120);   // [512] scalar V path (V phase)
-  float* qsm = (float*)(wsm + 4096);           // [G][128] residue chunks (q copy)
-  float* sbuf = (float*)(wsm + kTileA);        // [GP][64] scores, then p
+  float* sbuf = (float*)wsm;                   // [GP][64] the item's scores, then p (until the item ends)
+  uint8_t* frag = wsm + 2048;                  // [GP][2][64] V B operand
+  float* vtmp = (float*)(wsm + 3072);          // [GP][128] a scalar-path / residue V sum (channel per lane)
+  uint32_t* xdesc = (uint32_t*)(wsm + 3072);   // [512] scalar-path descriptors (before vtmp is written)
+  float* qsm = (float*)(wsm + 3072);           // [G][128] residue chunks: the q copy (K step)
   FeedA F;
-  F.init(wsm + kTileA + 2048, lane);
+  F.init(wsm + kTileA, lane);
   F.NI = NI;
   __syncthreads();
   const uint32_t tile_s = smem_u32(tile);
@@ -88,12 +97,21 @@ __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
   const uint32_t st_even = 16u * ((R0 & ~7u) | ((R0 & 7u) ^ X));
   const uint32_t st_odd = 16u * ((R0 & ~7u) | (((R0 & 7u) | 4u) ^ X));
   const int64_t nwarps = int64_t(gridDim.x) * kWA, wid = int64_t(blockIdx.x) * kWA + warp;
-  const Range rg = warp_range(total, wid, nwarps);
-  const int nk = int(rg.b1 - rg.b0);
+  // Work split: the item sequence is cut into `nchunks` equal contiguous
+  // ranges (chunks), chunk c on warp c mod nwarps (nchunks = nwarps: one
+  // contiguous range per warp).  Partial slots are per (unit, chunk).  (Taking
+  // chunks from an atomic counter measured slower: every chunk start pays the
+  // directory, query-fragment and first-block latencies.)
+  int64_t cw = 0;  // current chunk
+  Range rg;
   // writer role (softmax step and the V B operand): head wh, rows wt0 .. wt0 + TPL - 1
   const int wh = lane / LPH, wt0 = (lane % LPH) * TPL;
 
+#if PKV_Q2
+  QFrag2<NG> Q;
+#else
   QFrag<NG> Q;
+#endif
   float acc[NG][16];
   float Mw = -INFINITY, lacc = 0.f, zacc = 0.f;  // writer head wh: running max (log2), sum p, sum p z
 #pragma unroll
@@ -103,9 +121,9 @@ __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
 
   // ---- partial of unit u (this warp's segment), then the merge by the last arriver
   auto flush = [&](int u) {
-    const int64_t w0 = warp_of(int64_t(u) * NI, total, nwarps);
-    const int64_t w1 = warp_of(int64_t(u + 1) * NI - 1, total, nwarps);
-    float* pp = part + (int64_t(u) * maxseg + (wid - w0)) * G * kPartA;
+    const int64_t w0 = warp_of(int64_t(u) * NI, total, nchunks);
+    const int64_t w1 = warp_of(int64_t(u + 1) * NI - 1, total, nchunks);
+    float* pp = part + (int64_t(u) * maxseg + (cw - w0)) * G * kPartA;
 #pragma unroll
     for (int nt = 0; nt < NG; ++nt) {
       const int g = 4 * nt + tq;
@@ -131,6 +149,7 @@ __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
     }
     Mw = -INFINITY;
     lacc = zacc = 0.f;
+    if (cnt == nullptr) return;  // attn_merge_kernel merges
     __threadfence();
     __syncwarp();
     int last = 0;
@@ -142,28 +161,61 @@ __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
     const float* pu = part + int64_t(u) * maxseg * G * kPartA;
     const int64_t st = int64_t(G) * kPartA;
     const int b = u / L.heads, h = u - b * L.heads;
-    for (int g = 0; g < G; ++g) {
-      float m = -INFINITY;
-      for (int s = lane; s < ns; s += 32) m = fmaxf(m, ldcg_f(pu + s * st + g * kPartA + kD + 2));
-      m = warp_max(m);
-      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-      float zs = 0.f, ls = 0.f;
-#pragma unroll 4
-      for (int s = 0; s < ns; ++s) {
-        const float* ps = pu + s * st + g * kPartA;
-        const float Ms = ldcg_f(ps + kD + 2);
-        const float e = Ms == -INFINITY ? 0.f : exp2f(Ms - m);
-        const float4 a = __ldcg((const float4*)(ps + 4 * lane));
-        o.x = fmaf(e, a.x, o.x);
-        o.y = fmaf(e, a.y, o.y);
-        o.z = fmaf(e, a.z, o.z);
-        o.w = fmaf(e, a.w, o.w);
-        zs = fmaf(e, ldcg_f(ps + kD), zs);
-        ls = fmaf(e, ldcg_f(ps + kD + 1), ls);
+    // every head at once (independent loads in flight): slot statistics with
+    // lane s holding slots s, s + 32, ..., then the channel sums in slot order
+    float m[GP], zs[GP], ls[GP];
+#pragma unroll
+    for (int g = 0; g < GP; ++g) m[g] = -INFINITY;
+    for (int s = lane; s < ns; s += 32)
+#pragma unroll
+      for (int g = 0; g < GP; ++g)
+        if (g < G) m[g] = fmaxf(m[g], ldcg_f(pu + s * st + g * kPartA + kD + 2));
+#pragma unroll
+    for (int g = 0; g < GP; ++g) {
+      m[g] = warp_max(m[g]);
+      zs[g] = ls[g] = 0.f;
+    }
+    float4 o[GP];
+#pragma unroll
+    for (int g = 0; g < GP; ++g) o[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < ns; s0 += 32) {
+      const int sl = s0 + lane;
+      float el[GP];
+#pragma unroll
+      for (int g = 0; g < GP; ++g) {
+        el[g] = 0.f;
+        if (g < G && sl < ns) {
+          const float* ps = pu + sl * st + g * kPartA;
+          const float Ms = ldcg_f(ps + kD + 2);
+          el[g] = Ms == -INFINITY ? 0.f : exp2f(Ms - m[g]);
+          zs[g] = fmaf(el[g], ldcg_f(ps + kD), zs[g]);
+          ls[g] = fmaf(el[g], ldcg_f(ps + kD + 1), ls[g]);
+        }
       }
-      const float inv = ls > 0.f ? 1.f / ls : 0.f;
+      const int n = min(32, ns - s0);
+#pragma unroll 4
+      for (int i = 0; i < n; ++i) {
+        const float* ps = pu + (s0 + i) * st + 4 * lane;
+#pragma unroll
+        for (int g = 0; g < GP; ++g) {
+          const float e = __shfl_sync(PKV_FULL, el[g], i);
+          if (g < G) {
+            const float4 a = __ldcg((const float4*)(ps + g * kPartA));
+            o[g].x = fmaf(e, a.x, o[g].x);
+            o[g].y = fmaf(e, a.y, o[g].y);
+            o[g].z = fmaf(e, a.z, o[g].z);
+            o[g].w = fmaf(e, a.w, o[g].w);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < GP; ++g) {
+      if (g >= G) continue;
+      const float z = warp_sum(zs[g]), l = warp_sum(ls[g]);
+      const float inv = l > 0.f ? 1.f / l : 0.f;
       *(float4*)(out + (int64_t(b) * Hq + int64_t(h) * G + g) * kD + 4 * lane) =
-          make_float4((o.x + zs) * inv, (o.y + zs) * inv, (o.z + zs) * inv, (o.w + zs) * inv);
+          make_float4((o[g].x + z) * inv, (o[g].y + z) * inv, (o[g].z + z) * inv, (o[g].w + z) * inv);
     }
     if (lane == 0) cnt[u] = 0;  // ready for the next launch
   };
@@ -230,154 +282,297 @@ __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
     __syncwarp();
   };
 
+  int cur_u = -1, b = 0, h = 0;
+#if PKV_ADIAG
+  long long dg[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // wait K, wait V, K phase, V phase, all, items, end refill, unit change
+  const long long dg0 = clock64();
+  long long dgt = 0;
+  int nitems = 0;
+#endif
+#pragma unroll 1
+  for (cw = wid; cw < nchunks; cw += nwarps) {
+  rg = warp_range(total, cw, nchunks);
+  const int nk = int(rg.b1 - rg.b0);
+#if PKV_ADIAG
+  nitems += nk;
+#endif
+  // feed indices continue across chunks (the ring's mbarrier phases do)
+  const int fb = F.issued;
+  F.base = fb;
+  F.k0 = fb - 32;
   Cursor cs;
   cs.init(rg.b0, NI, L.heads);
-  int cur_u = -1, b = 0, h = 0;
-  F.refill(L, 0, NB, rg, 2 * nk, -1, 0u, lane);
+  cur_u = -1;
+  F.refill(L, 0, NB, rg, fb + 2 * nk, fb - 1, F.head, lane);
 
 #pragma unroll 1
   for (int k = 0; k < nk; ++k, cs.step(1, NI, L.heads)) {
     const int u = cs.u, j = cs.j;
     if (u != cur_u) {
+#if PKV_ADIAG
+      const long long tu = clock64();
+#endif
       if (cur_u >= 0) flush(cur_u);
       cur_u = u;
       b = cs.b;
       h = cs.h;
       build_qfrag<NG>(q + (int64_t(b) * Hq + int64_t(h) * G) * kD, G, lane, Q);
+#if PKV_ADIAG
+      dg[7] += clock64() - tu;
+#endif
     }
-    // ================================================================ K phase
-    const uint8_t* gk;
-    bool have_k;
-    const uint32_t kblk = F.wait(2 * k, &gk, &have_k);
-    bool rows = false;  // the item holds at least one token
-    int nres = 0, r0 = 0;
+    const int src = 8 * tq + gi;  // V: the chunk this lane decodes (row-group tq, channels 16gi ..)
     if (j < NB) {
-      if (have_k) {
-        rows = true;
-        Chunk ch;
-        auto fast_block = [&](auto bp) {
-          auto decode_packs = [&](auto wide) {
-            uint32_t bit = ch.bit;
-            uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
-            PackLd A = pack_load<PKV_KREGC>(bp, lutb, bit, wa), B = pack_load<PKV_KREGC>(bp, lutb, bit + wa, wb);
+      // ============================ block item: K phase, softmax step, V phase.
+      // ONE decode loop serves both phases (ph 0: K codes into the transpose
+      // tile; ph 1: V codes straight into the IMMA A operand): two unrolled
+      // decode loops overflow the 32 KB L1.5 instruction cache (ncu: ~1.2
+      // no-instruction stalls per issue against ~0.17 for the K or V kernel).
+#pragma unroll 1
+      for (int ph = 0; ph < 2; ++ph) {
+        const uint8_t* gb;
+        bool have;
+#if PKV_ADIAG
+        dgt = clock64();
+#endif
+        const uint32_t sb = F.wait(fb + 2 * k + ph, &gb, &have);
+#if PKV_ADIAG
+        { const long long t1 = clock64(); dg[ph] += t1 - dgt; dgt = t1; }
+#endif
+        if (!have) break;  // past the sequence's block count: K and V both absent
+        auto phase = [&](auto bp, bool may_fast_v) {
+          Chunk ch;
+          bool fast;
+          uint32_t bf[NG][4];
+          float inv[NG];
+          if (ph == 0) {
+            fast = parse_chunk(bp, lane, lane, ch);
+          } else {
+            // B operand: x_t = p_t * s_t as 2 unsigned byte digits scaled per
+            // (block, head) (fused_v_fast_kernel), z term sum p_t z_t in f32
+            parse_load(bp, lane, src, ch);
+            uint2 pr[TPL / 2];
 #pragma unroll
-            for (int i2 = 0; i2 < 16; i2 += 2) {
-              const uint32_t bitA = bit, bitB = bit + wa;
-              const uint32_t nbit = bitB + wb;
-              uint32_t nwa = 0, nwb = 0;
-              PackLd nA, nB;
-              if (i2 < 14) {
-                nwa = w16_of(ch.nb, i2 + 2);
-                nwb = w16_of(ch.nb, i2 + 3);
-                nA = pack_load<PKV_KREGC>(bp, lutb, nbit, nwa);
-                nB = pack_load<PKV_KREGC>(bp, lutb, nbit + nwa, nwb);
+            for (int e2 = 0; e2 < TPL / 2; ++e2) pr[e2] = ld64(bp + kPar + 4 * (wt0 + 2 * e2));
+            float wc[TPL];
+#pragma unroll
+            for (int e4 = 0; e4 < TPL / 4; ++e4) {
+              const float4 v = *(const float4*)(sbuf + wh * 64 + wt0 + 4 * e4);
+              wc[4 * e4] = v.x; wc[4 * e4 + 1] = v.y; wc[4 * e4 + 2] = v.z; wc[4 * e4 + 3] = v.w;
+            }
+            float xs[TPL];
+            float mx = 0.f;
+            bool neg = false;
+#pragma unroll
+            for (int e2 = 0; e2 < TPL / 2; ++e2) {
+              const float s0 = h2f(pr[e2].x & 0xffff), s1 = h2f(pr[e2].y & 0xffff);
+              zacc = fmaf(wc[2 * e2], h2f(pr[e2].x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr[e2].y >> 16), zacc));
+              xs[2 * e2] = wc[2 * e2] * s0;
+              xs[2 * e2 + 1] = wc[2 * e2 + 1] * s1;
+              mx = fmaxf(mx, fmaxf(xs[2 * e2], xs[2 * e2 + 1]));
+              neg |= (xs[2 * e2] < 0.f) | (xs[2 * e2 + 1] < 0.f);
+            }
+            const uint32_t flags = parse_flags(ch) | (neg ? uint32_t(kFNeg) : 0u);
+            fast = parse_verdict(__reduce_or_sync(PKV_FULL, flags), ch) && may_fast_v;
+            parse_scan(lane, ch);
+#pragma unroll
+            for (int o = 1; o < LPH; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(PKV_FULL, mx, o));
+            const float f = mx > 1e-30f ? __fdividef(65535.f, mx) : 0.f;
+            const float invf = mx * (1.f / 65535.f);
+            if (fast) {
+#pragma unroll
+              for (int e8 = 0; e8 < TPL / 8; ++e8) {
+                uint32_t v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = min(__float_as_uint(__fmaf_rn(xs[8 * e8 + e], f, 8388608.f)), 0x4B00FFFFu);
+                const uint32_t t01 = __byte_perm(v[0], v[1], 0x5140), t45 = __byte_perm(v[4], v[5], 0x5140);
+                const uint32_t t23 = __byte_perm(v[2], v[3], 0x5140), t67 = __byte_perm(v[6], v[7], 0x5140);
+                const uint32_t lo0 = __byte_perm(t01, t45, 0x5410), hi0 = __byte_perm(t01, t45, 0x7632);
+                const uint32_t lo1 = __byte_perm(t23, t67, 0x5410), hi1 = __byte_perm(t23, t67, 0x7632);
+                *(uint2*)(frag + (wh * 2 + 0) * 64 + wt0 + 8 * e8) = make_uint2(lo0, lo1);
+                *(uint2*)(frag + (wh * 2 + 1) * 64 + wt0 + 8 * e8) = make_uint2(hi0, hi1);
               }
-              uint32_t ra[4], rb[4];
-              pack_decode<decltype(wide)::value>(bp, A, bitA, wa, min_rep(ch.mn, i2), ra);
-              pack_decode<decltype(wide)::value>(bp, B, bitB, wb, min_rep(ch.mn, i2 + 1), rb);
-              *(uint4*)(tile + st_even + 128u * (i2 >> 1)) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
-              *(uint4*)(tile + st_odd + 128u * (i2 >> 1)) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
-              bit = nbit;
-              wa = nwa;
-              wb = nwb;
-              if (i2 < 14) {
-                A = nA;
-                B = nB;
+              __syncwarp();
+#pragma unroll
+              for (int nt = 0; nt < NG; ++nt) {
+                const uint4 v = *(const uint4*)(frag + ((4 * nt + (gi >> 1)) * 2 + (gi & 1)) * 64 + 16 * tq);
+                bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
+                inv[nt] = __shfl_sync(PKV_FULL, invf, (4 * nt + tq) * LPH);
               }
             }
-          };
-          if (ch.wide) decode_packs(std::true_type{});
-          else decode_packs(std::false_type{});
-          uint32_t prm[4][2];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            prm[g][0] = ld32(bp + kPar + 4 * (16 * g + tok(gi)));
-            prm[g][1] = ld32(bp + kPar + 4 * (16 * g + tok(gi) + 8));
           }
-          __syncwarp();
-          float* s0 = sbuf + tq * 64 + tok(gi);  // rows 16g + tok(gi) (+8) of head tq (+4)
+          if (fast) {
+            // lane walks chunk cidx: its own (K: the transpose tile's order) or
+            // chunk 8tq + gi (V: the A fragment's order); minima of that chunk are in ch.mn
+            const int cidx = ph ? src : lane;
+            uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, cidx);
+            const uint2 nb = ph ? ld64(bp + kNib + 8 * src) : ch.nb;
+            auto decode = [&](auto wide) {
+              uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
+              PackLd A = pack_load<PKV_AREGC>(bp, lutb, bit, wa), B = pack_load<PKV_AREGC>(bp, lutb, bit + wa, wb);
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            int accU[NG][4], accS[4];
+              for (int mt = 0; mt < 8; ++mt) {
+                uint32_t P[2][4];
+                const int i2 = 2 * mt;
+                const uint32_t bitA = bit, bitB = bit + wa;
+                const uint32_t nbit = bitB + wb;
+                uint32_t nwa = 0, nwb = 0;
+                PackLd nA, nB;
+                if (i2 < 14) {
+                  nwa = w16_of(nb, i2 + 2);
+                  nwb = w16_of(nb, i2 + 3);
+                  nA = pack_load<PKV_AREGC>(bp, lutb, nbit, nwa);
+                  nB = pack_load<PKV_AREGC>(bp, lutb, nbit + nwa, nwb);
+                }
+                pack_decode<decltype(wide)::value>(bp, A, bitA, wa, min_rep(ch.mn, i2), P[0]);
+                pack_decode<decltype(wide)::value>(bp, B, bitB, wb, min_rep(ch.mn, i2 + 1), P[1]);
+                bit = nbit;
+                wa = nwa;
+                wb = nwb;
+                if (i2 < 14) {
+                  A = nA;
+                  B = nB;
+                }
+                if (ph == 0) {
+                  *(uint4*)(tile + st_even + 128u * mt) = make_uint4(P[0][0], P[0][1], P[0][2], P[0][3]);
+                  *(uint4*)(tile + st_odd + 128u * mt) = make_uint4(P[1][0], P[1][1], P[1][2], P[1][3]);
+                } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              accS[e] = 0;
-#pragma unroll
-              for (int nu = 0; nu < NG; ++nu) accU[nu][e] = 0;
-            }
-            const uint32_t a0 = tile_s + 16u * (128u * g + lane);
-            const uint32_t a1 = tile_s + 16u * (128u * g + (lane ^ 4u) + 64u);
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              uint32_t a[4];
-              ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
-#pragma unroll
-              for (int nu = 0; nu < NG; ++nu) imma_uu(accU[nu], a, Q.u[nu][jj][0], Q.u[nu][jj][1]);
-              imma_us(accS, a, Q.s[jj][0], Q.s[jj][1]);
-            }
-            const float sA = h2f(prm[g][0] & 0xffff), zA = h2f(prm[g][0] >> 16);
-            const float sB = h2f(prm[g][1] & 0xffff), zB = h2f(prm[g][1] >> 16);
-            {
-              const float vA = fmaf(65536.f, float(accS[0]), float(accU[0][0] + 256 * accU[0][1]));
-              const float vB = fmaf(65536.f, float(accS[2]), float(accU[0][2] + 256 * accU[0][3]));
-              s0[16 * g] = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]);
-              s0[16 * g + 8] = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
-            }
-            if (NG == 2) {
-              const float vA = fmaf(65536.f, float(accS[1]), float(accU[NG - 1][0] + 256 * accU[NG - 1][1]));
-              const float vB = fmaf(65536.f, float(accS[3]), float(accU[NG - 1][2] + 256 * accU[NG - 1][3]));
-              s0[256 + 16 * g] = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]);
-              s0[256 + 16 * g + 8] = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
-            }
-          }
-          __syncwarp();  // tile reads done
-        };
-        bool fast;
-        if (gk == nullptr) {
-          fast = parse_chunk(kblk, lane, lane, ch);
-          if (fast) fast_block(kblk);
-        } else {
-          fast = parse_chunk(gk, lane, lane, ch);
-          if (fast) fast_block(gk);
-        }
-        if (!fast) {
-          // scalar path (rare): lane computes rows lane and lane + 32 for every head
-          const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
-          uint32_t* desc = (uint32_t*)tile;
-          const uint8_t* bg = gk ? gk : gptr(kblk);
-          if (gk) parse_chunk(bg, lane, lane, ch);
-          build_desc(ch, lane, desc);
-#pragma unroll 1
-          for (int half = 0; half < 2; ++half) {
-            const int tt = lane + 32 * half, rgp = tt >> 4, t16 = tt & 15;
-            const uint32_t pr = ld32(bg + kPar + 4 * tt);
-            const float s = h2f(pr & 0xffff), z = h2f(pr >> 16);
-#pragma unroll 1
-            for (int g = 0; g < GP; ++g) {
-              float a = 0.f, qsum = 0.f;
-              if (g < G) {
-#pragma unroll 1
-                for (int pos = 0; pos < 128; ++pos) {
-                  const uint32_t d = desc[rgp * 128 + pos];
-                  const uint32_t wd = d >> 18;
-                  const float code = float(pack_min(bg, rgp * 128 + pos) + field_at(bg, (d & 0x3ffffu) + t16 * wd, wd));
-                  const float qc = qu[g * kD + kpos_to_col(pos, kD)];
-                  a = fmaf(code, qc, a);
-                  qsum += qc;
+                  for (int nt = 0; nt < NG; ++nt) {
+                    int d[4] = {0, 0, 0, 0};
+                    const uint32_t a0[4] = {P[0][0], P[1][0], P[0][1], P[1][1]};
+                    imma_uu(d, a0, bf[nt][0], bf[nt][1]);
+                    const uint32_t a1[4] = {P[0][2], P[1][2], P[0][3], P[1][3]};
+                    imma_uu(d, a1, bf[nt][2], bf[nt][3]);
+                    acc[nt][2 * mt] = fmaf(float(d[0] + 256 * d[1]), inv[nt], acc[nt][2 * mt]);
+                    acc[nt][2 * mt + 1] = fmaf(float(d[2] + 256 * d[3]), inv[nt], acc[nt][2 * mt + 1]);
+                  }
                 }
               }
-              sbuf[g * 64 + tt] = fmaf(s, a, z * qsum);
+            };
+            if (ch.wide) decode(std::true_type{});
+            else decode(std::false_type{});
+            __syncwarp();  // tile stores (K) / frag reads (V) done
+            if (ph == 0) {
+              // scores of rows 16g + tok(gi) (+8), heads tq (+4), into sbuf (row-group 0 of the tile)
+              float* s0 = sbuf + tq * 64 + tok(gi);
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                int accU[NG][4], accS[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  accS[e] = 0;
+#pragma unroll
+                  for (int nu = 0; nu < NG; ++nu) accU[nu][e] = 0;
+                }
+                const uint32_t prA = ld32(bp + kPar + 4 * (16 * g + tok(gi)));
+                const uint32_t prB = ld32(bp + kPar + 4 * (16 * g + tok(gi) + 8));
+                const uint32_t a0 = tile_s + 16u * (128u * g + lane);
+                const uint32_t a1 = tile_s + 16u * (128u * g + (lane ^ 4u) + 64u);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  uint32_t a[4];
+                  ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
+                  k_mma<NG>(accU, accS, a, Q, jj);
+                }
+                if (g == 0) __syncwarp();  // every lane has read row-group 0 (sbuf's bytes)
+                const float sA = h2f(prA & 0xffff), zA = h2f(prA >> 16);
+                const float sB = h2f(prB & 0xffff), zB = h2f(prB >> 16);
+                {
+                  const float vA = k_val<NG>(accU, accS, Q, 0, 0);
+                  const float vB = k_val<NG>(accU, accS, Q, 0, 1);
+                  s0[16 * g] = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]);
+                  s0[16 * g + 8] = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
+                }
+                if (NG == 2) {
+                  const float vA = k_val<NG>(accU, accS, Q, NG - 1, 0);
+                  const float vB = k_val<NG>(accU, accS, Q, NG - 1, 1);
+                  s0[256 + 16 * g] = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]);
+                  s0[256 + 16 * g + 8] = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
+                }
+              }
             }
+          } else if (ph == 0) {
+            // scalar K (rare): lane computes rows lane and lane + 32 for every head
+            const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
+            const uint8_t* bg = gptr(bp);
+            build_desc(ch, lane, xdesc);
+#pragma unroll 1
+            for (int half = 0; half < 2; ++half) {
+              const int tt = lane + 32 * half, rgp = tt >> 4, t16 = tt & 15;
+              const uint32_t prr = ld32(bg + kPar + 4 * tt);
+              const float s = h2f(prr & 0xffff), z = h2f(prr >> 16);
+#pragma unroll 1
+              for (int g = 0; g < GP; ++g) {
+                float a = 0.f, qsum = 0.f;
+                if (g < G) {
+#pragma unroll 1
+                  for (int pos = 0; pos < 128; ++pos) {
+                    const uint32_t d = xdesc[rgp * 128 + pos];
+                    const uint32_t wd = d >> 18;
+                    const float code = float(pack_min(bg, rgp * 128 + pos) + field_at(bg, (d & 0x3ffffu) + t16 * wd, wd));
+                    const float qc = qu[g * kD + kpos_to_col(pos, kD)];
+                    a = fmaf(code, qc, a);
+                    qsum += qc;
+                  }
+                }
+                sbuf[g * 64 + tt] = fmaf(s, a, z * qsum);
+              }
+            }
+          } else {
+            // scalar V (rare): lane owns channels lane + 32 q4, all 64 rows, every
+            // head; the block's sum goes through vtmp into acc
+            const uint8_t* bg = gptr(bp);
+            build_desc(ch, lane, xdesc);
+            float sacc[GP][4];
+#pragma unroll
+            for (int g = 0; g < GP; ++g)
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) sacc[g][q4] = 0.f;
+#pragma unroll 1
+            for (int r = 0; r < kRows; ++r) {
+              const uint32_t prr = ld32(bg + kPar + 4 * r);
+              const float s = h2f(prr & 0xffff);
+              float ws[GP];
+#pragma unroll
+              for (int g = 0; g < GP; ++g) ws[g] = sbuf[g * 64 + r] * s;
+              const int rgp = r >> 4, tt = r & 15;
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                const int c = lane + 32 * q4;
+                const uint32_t dd = xdesc[rgp * 128 + c];
+                const uint32_t wd = dd >> 18;
+                const float code = float(pack_min(bg, rgp * 128 + c) + field_at(bg, (dd & 0x3ffffu) + tt * wd, wd));
+#pragma unroll
+                for (int g = 0; g < GP; ++g) sacc[g][q4] = fmaf(ws[g], code, sacc[g][q4]);
+              }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < GP; ++g)
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) vtmp[g * kD + lane + 32 * q4] = sacc[g][q4];
+            add_vtmp();
           }
-          __syncwarp();
+        };
+        if (gb)
+          phase(gb, false);  // too large for the ring: read in place (V takes the scalar path)
+        else
+          phase(sb, true);
+        if (ph == 0) {
+          // the K block's ring bytes are free: top up the feed while V runs
+          F.refill(L, 0, NB, rg, fb + 2 * nk, fb + 2 * k, F.tail_after(fb + 2 * k), lane);
+          softmax_step();
         }
+#if PKV_ADIAG
+        dg[2 + ph] += clock64() - dgt;
+#endif
       }
     } else {
-      // residue chunk: staged rows r0 .. r0 + 31 of the unit (fp16, f32 SIMT)
-      r0 = (j - NB) * kResRows;
-      nres = min(L.nres[b] - r0, kResRows);
+      // ============================ residue chunk: staged rows r0 .. r0 + 31 (fp16, f32 SIMT)
+      const int r0 = (j - NB) * kResRows;
+      const int nres = min(L.nres[b] - r0, kResRows);
       if (nres > 0) {
-        rows = true;
         const float* qu = q + (int64_t(b) * Hq + int64_t(h) * G) * kD;
         __syncwarp();
         for (int i = lane; i < G * kD / 4; i += 32) reinterpret_cast<float4*>(qsm)[i] = reinterpret_cast<const float4*>(qu)[i];
@@ -403,189 +598,131 @@ __global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
             }
           }
         }
+        __syncwarp();  // qsm reads done (sbuf and vtmp follow)
 #pragma unroll
         for (int g = 0; g < GP; ++g) {
           sbuf[g * 64 + lane] = lane < nres ? a[g] : -INFINITY;
           sbuf[g * 64 + 32 + lane] = -INFINITY;
         }
-      }
-    }
-    // the K block's ring bytes are free: top up the feed while V runs
-    F.refill(L, 0, NB, rg, 2 * nk, 2 * k, F.tail_after(2 * k), lane);
-    if (rows) softmax_step();
-
-    // ================================================================ V phase
-    const uint8_t* gv;
-    bool have_v;
-    const uint32_t vsb = F.wait(2 * k + 1, &gv, &have_v);
-    if (rows && j < NB && have_v) {
-      auto process = [&](auto blk, bool may_fast) {
-        Chunk ch;
-        const int src = 8 * tq + gi;
-        parse_load(blk, lane, src, ch);
-        uint2 pr[TPL / 2];
+        softmax_step();
+        // out[g][c] += sum_t p[g][t] v[t][c], lane owns channels 4 lane .. + 3
+        float av[GP][4];
 #pragma unroll
-        for (int e2 = 0; e2 < TPL / 2; ++e2) pr[e2] = ld64(blk + kPar + 4 * (wt0 + 2 * e2));
-        float wc[TPL];
-#pragma unroll
-        for (int e4 = 0; e4 < TPL / 4; ++e4) {
-          const float4 v = *(const float4*)(sbuf + wh * 64 + wt0 + 4 * e4);
-          wc[4 * e4] = v.x; wc[4 * e4 + 1] = v.y; wc[4 * e4 + 2] = v.z; wc[4 * e4 + 3] = v.w;
-        }
-        float xs[TPL];
-        float mx = 0.f;
-        bool neg = false;
-#pragma unroll
-        for (int e2 = 0; e2 < TPL / 2; ++e2) {
-          const float s0 = h2f(pr[e2].x & 0xffff), s1 = h2f(pr[e2].y & 0xffff);
-          zacc = fmaf(wc[2 * e2], h2f(pr[e2].x >> 16), fmaf(wc[2 * e2 + 1], h2f(pr[e2].y >> 16), zacc));
-          xs[2 * e2] = wc[2 * e2] * s0;
-          xs[2 * e2 + 1] = wc[2 * e2 + 1] * s1;
-          mx = fmaxf(mx, fmaxf(xs[2 * e2], xs[2 * e2 + 1]));
-          neg |= (xs[2 * e2] < 0.f) | (xs[2 * e2 + 1] < 0.f);
-        }
-        const uint32_t flags = parse_flags(ch) | (neg ? uint32_t(kFNeg) : 0u);
-        const bool fast = parse_verdict(__reduce_or_sync(PKV_FULL, flags), ch) && may_fast;
-        parse_scan(lane, ch);
-#pragma unroll
-        for (int o = 1; o < LPH; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(PKV_FULL, mx, o));
-        const float f = mx > 1e-30f ? __fdividef(65535.f, mx) : 0.f;
-        const float invf = mx * (1.f / 65535.f);
-        if (fast) {
-#pragma unroll
-          for (int e8 = 0; e8 < TPL / 8; ++e8) {
-            uint32_t v[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = min(__float_as_uint(__fmaf_rn(xs[8 * e8 + e], f, 8388608.f)), 0x4B00FFFFu);
-            const uint32_t t01 = __byte_perm(v[0], v[1], 0x5140), t45 = __byte_perm(v[4], v[5], 0x5140);
-            const uint32_t t23 = __byte_perm(v[2], v[3], 0x5140), t67 = __byte_perm(v[6], v[7], 0x5140);
-            const uint32_t lo0 = __byte_perm(t01, t45, 0x5410), hi0 = __byte_perm(t01, t45, 0x7632);
-            const uint32_t lo1 = __byte_perm(t23, t67, 0x5410), hi1 = __byte_perm(t23, t67, 0x7632);
-            *(uint2*)(frag + (wh * 2 + 0) * 64 + wt0 + 8 * e8) = make_uint2(lo0, lo1);
-            *(uint2*)(frag + (wh * 2 + 1) * 64 + wt0 + 8 * e8) = make_uint2(hi0, hi1);
-          }
-          __syncwarp();
-          uint32_t bf[NG][4];
-          float inv[NG];
-#pragma unroll
-          for (int nt = 0; nt < NG; ++nt) {
-            const uint4 v = *(const uint4*)(frag + ((4 * nt + (gi >> 1)) * 2 + (gi & 1)) * 64 + 16 * tq);
-            bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
-            inv[nt] = __shfl_sync(PKV_FULL, invf, (4 * nt + tq) * LPH);
-          }
-          uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src);
-          const uint2 nb = ld64(blk + kNib + 8 * src);
-          const uint32_t (&mn)[8] = ch.mn;
-          auto decode_mma = [&](auto wide) {
-            uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
-            PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-              uint32_t P[2][4];
-              {
-                const int i2 = 2 * mt;
-                const uint32_t bitA = bit, bitB = bit + wa;
-                const uint32_t nbit = bitB + wb;
-                uint32_t nwa = 0, nwb = 0;
-                PackLd nA, nB;
-                if (i2 < 14) {
-                  nwa = w16_of(nb, i2 + 2);
-                  nwb = w16_of(nb, i2 + 3);
-                  nA = pack_load(blk, lutb, nbit, nwa);
-                  nB = pack_load(blk, lutb, nbit + nwa, nwb);
-                }
-                pack_decode<decltype(wide)::value>(blk, A, bitA, wa, min_rep(mn, i2), P[0]);
-                pack_decode<decltype(wide)::value>(blk, B, bitB, wb, min_rep(mn, i2 + 1), P[1]);
-                bit = nbit;
-                wa = nwa;
-                wb = nwb;
-                if (i2 < 14) {
-                  A = nA;
-                  B = nB;
-                }
-              }
-#pragma unroll
-              for (int nt = 0; nt < NG; ++nt) {
-                int d[4] = {0, 0, 0, 0};
-                const uint32_t a0[4] = {P[0][0], P[1][0], P[0][1], P[1][1]};
-                imma_uu(d, a0, bf[nt][0], bf[nt][1]);
-                const uint32_t a1[4] = {P[0][2], P[1][2], P[0][3], P[1][3]};
-                imma_uu(d, a1, bf[nt][2], bf[nt][3]);
-                acc[nt][2 * mt] = fmaf(float(d[0] + 256 * d[1]), inv[nt], acc[nt][2 * mt]);
-                acc[nt][2 * mt + 1] = fmaf(float(d[2] + 256 * d[3]), inv[nt], acc[nt][2 * mt + 1]);
-              }
-            }
-          };
-          if (ch.wide) decode_mma(std::true_type{});
-          else decode_mma(std::false_type{});
-          __syncwarp();  // frag reads done before the next block's tile stores
-        } else {
-          // scalar path (rare): lane owns channels lane + 32 q4, all 64 rows, every
-          // head; the block's sum goes through vtmp into acc
-          const uint8_t* bg = gptr(blk);
-          build_desc(ch, lane, vdesc);
-          float sacc[GP][4];
-#pragma unroll
-          for (int g = 0; g < GP; ++g)
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) sacc[g][q4] = 0.f;
-#pragma unroll 1
-          for (int r = 0; r < kRows; ++r) {
-            const uint32_t prr = ld32(bg + kPar + 4 * r);
-            const float s = h2f(prr & 0xffff);
-            float ws[GP];
-#pragma unroll
-            for (int g = 0; g < GP; ++g) ws[g] = sbuf[g * 64 + r] * s;
-            const int rgp = r >> 4, tt = r & 15;
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const int c = lane + 32 * q4;
-              const uint32_t dd = vdesc[rgp * 128 + c];
-              const uint32_t wd = dd >> 18;
-              const float code = float(pack_min(bg, rgp * 128 + c) + field_at(bg, (dd & 0x3ffffu) + tt * wd, wd));
-#pragma unroll
-              for (int g = 0; g < GP; ++g) sacc[g][q4] = fmaf(ws[g], code, sacc[g][q4]);
-            }
-          }
-          __syncwarp();
-#pragma unroll
-          for (int g = 0; g < GP; ++g)
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) vtmp[g * kD + lane + 32 * q4] = sacc[g][q4];
-          add_vtmp();
-        }
-      };
-      if (gv)
-        process(gv, false);
-      else
-        process(F.ring + (vsb - smem_u32(F.ring)), true);
-    } else if (rows && j >= NB) {
-      // residue chunk: out[g][c] += sum_t p[g][t] v[t][c], lane owns channels 4 lane .. + 3
-      float a[GP][4];
-#pragma unroll
-      for (int g = 0; g < GP; ++g) a[g][0] = a[g][1] = a[g][2] = a[g][3] = 0.f;
-      const uint16_t* vr = L.stage + ((int64_t(U) + u) * L.buffer + r0) * kD + 4 * lane;
+        for (int g = 0; g < GP; ++g) av[g][0] = av[g][1] = av[g][2] = av[g][3] = 0.f;
+        const uint16_t* vr = L.stage + ((int64_t(U) + u) * L.buffer + r0) * kD + 4 * lane;
 #pragma unroll 2
-      for (int t = 0; t < nres; ++t) {
-        const uint2 v = *reinterpret_cast<const uint2*>(vr + int64_t(t) * kD);
-        const float x0 = h2f(v.x & 0xffff), x1 = h2f(v.x >> 16), x2 = h2f(v.y & 0xffff), x3 = h2f(v.y >> 16);
+        for (int t = 0; t < nres; ++t) {
+          const uint2 v = *reinterpret_cast<const uint2*>(vr + int64_t(t) * kD);
+          const float x0 = h2f(v.x & 0xffff), x1 = h2f(v.x >> 16), x2 = h2f(v.y & 0xffff), x3 = h2f(v.y >> 16);
 #pragma unroll
-        for (int g = 0; g < GP; ++g) {
-          const float p = sbuf[g * 64 + t];
-          a[g][0] = fmaf(p, x0, a[g][0]);
-          a[g][1] = fmaf(p, x1, a[g][1]);
-          a[g][2] = fmaf(p, x2, a[g][2]);
-          a[g][3] = fmaf(p, x3, a[g][3]);
+          for (int g = 0; g < GP; ++g) {
+            const float p = sbuf[g * 64 + t];
+            av[g][0] = fmaf(p, x0, av[g][0]);
+            av[g][1] = fmaf(p, x1, av[g][1]);
+            av[g][2] = fmaf(p, x2, av[g][2]);
+            av[g][3] = fmaf(p, x3, av[g][3]);
+          }
         }
-      }
-      __syncwarp();
+        __syncwarp();
 #pragma unroll
-      for (int g = 0; g < GP; ++g) *(float4*)(vtmp + g * kD + 4 * lane) = make_float4(a[g][0], a[g][1], a[g][2], a[g][3]);
-      add_vtmp();
+        for (int g = 0; g < GP; ++g) *(float4*)(vtmp + g * kD + 4 * lane) = make_float4(av[g][0], av[g][1], av[g][2], av[g][3]);
+        add_vtmp();
+      }
     }
-    F.refill(L, 0, NB, rg, 2 * nk, 2 * k + 1, F.tail_after(2 * k + 1), lane);
+#if PKV_ADIAG
+    const long long tr = clock64();
+#endif
+    F.refill(L, 0, NB, rg, fb + 2 * nk, fb + 2 * k + 1, F.tail_after(fb + 2 * k + 1), lane);
+#if PKV_ADIAG
+    dg[6] += clock64() - tr;
+#endif
   }
   if (cur_u >= 0) flush(cur_u);
+  }
+#if PKV_ADIAG
+  __syncwarp();
+  if (lane == 0) {
+    long long* dbg = reinterpret_cast<long long*>(out) + 8 * wid;
+    dg[4] = clock64() - dg0;
+    dg[5] = nitems;
+    for (int i = 0; i < 8; ++i) dbg[i] = dg[i];
+  }
+#endif
+}
+
+// The unit's slot partials merged in slot order (deterministic): one CTA of
+// 128 x kMQ threads per (unit, head); thread (q, c) folds slots q, q + kMQ, ...
+// of channel c with an online maximum, then the kMQ groups are combined in a
+// fixed order.  out = sum_s e^(M_s - M*) (acc_s + z_s) / sum_s e^(M_s - M*) l_s.
+constexpr int kMQ = 8;
+__global__ void __launch_bounds__(128 * kMQ) attn_merge_kernel(pkv_layer_t L, int G, int NI, int64_t total,
+                                                             int64_t nwarps, const float* __restrict__ part,
+                                                             int maxseg, float* __restrict__ out) {
+  __shared__ float rm[kMQ], rz[kMQ], rl[kMQ], ro[kMQ][kD];
+  const int c = threadIdx.x & 127, qq = threadIdx.x >> 7;
+  const int U = L.batch * L.heads, Hq = L.heads * G;
+  for (int ug = blockIdx.x; ug < U * G; ug += gridDim.x) {
+    const int u = ug / G, g = ug - u * G;
+    const int64_t w0 = warp_of(int64_t(u) * NI, total, nwarps), w1 = warp_of(int64_t(u + 1) * NI - 1, total, nwarps);
+    const int ns = int(w1 - w0 + 1);
+    const float* pg = part + (int64_t(u) * maxseg * G + g) * kPartA;
+    const int64_t st = int64_t(G) * kPartA;
+    float m = -INFINITY, o = 0.f, z = 0.f, l = 0.f;
+    auto fold = [&](float Ms, float a, float zs, float ls) {
+      if (Ms > m) {
+        const float sc = exp2f(m - Ms);  // m = -inf: 0
+        o *= sc;
+        z *= sc;
+        l *= sc;
+        m = Ms;
+      }
+      const float e = Ms == -INFINITY ? 0.f : exp2f(Ms - m);
+      o = fmaf(e, a, o);
+      z = fmaf(e, zs, z);
+      l = fmaf(e, ls, l);
+    };
+    int s = qq;
+    for (; s + 3 * kMQ < ns; s += 4 * kMQ) {  // four slots' loads in flight
+      float Mv[4], av[4], zv[4], lv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float* ps = pg + (s + i * kMQ) * st;
+        Mv[i] = ps[kD + 2];
+        av[i] = ps[c];
+        zv[i] = ps[kD];
+        lv[i] = ps[kD + 1];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fold(Mv[i], av[i], zv[i], lv[i]);
+    }
+    for (; s < ns; s += kMQ) {
+      const float* ps = pg + s * st;
+      fold(ps[kD + 2], ps[c], ps[kD], ps[kD + 1]);
+    }
+    ro[qq][c] = o;
+    if (c == 0) {
+      rm[qq] = m;
+      rz[qq] = z;
+      rl[qq] = l;
+    }
+    __syncthreads();
+    if (qq == 0) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kMQ; ++i) M = fmaxf(M, rm[i]);
+      float O = 0.f, Z = 0.f, Lw = 0.f;
+#pragma unroll
+      for (int i = 0; i < kMQ; ++i) {
+        const float e = rm[i] == -INFINITY ? 0.f : exp2f(rm[i] - M);
+        O = fmaf(e, ro[i][c], O);
+        Z = fmaf(e, rz[i], Z);
+        Lw = fmaf(e, rl[i], Lw);
+      }
+      const int b = u / L.heads, h = u - b * L.heads;
+      out[(int64_t(b) * Hq + int64_t(h) * G + g) * kD + c] = Lw > 0.f ? (O + Z) / Lw : 0.f;
+    }
+    __syncthreads();
+  }
 }
 
 constexpr size_t a_smem_bytes() { return 256 + kWA * kWarpSmemA; }
@@ -616,9 +753,12 @@ int attn_grid_cap(K kernel) {
   return cap;
 }
 
+#ifndef PKV_ACHUNKS  // work split: chunks per warp of the grid
+#define PKV_ACHUNKS 1
+#endif
 struct AttnPlan {
   int NB, NI, grid, maxseg, G;
-  int64_t total;
+  int64_t total, nchunks;
 };
 
 AttnPlan attn_plan(const pkv_layer_t* L, int nblocks, int G) {
@@ -632,35 +772,47 @@ AttnPlan attn_plan(const pkv_layer_t* L, int nblocks, int G) {
   const int64_t want = (p.total + kWA - 1) / kWA;
   p.grid = int(want < 1 ? 1 : (want < cap ? want : cap));
   const int64_t nwarps = int64_t(p.grid) * kWA;
-  // slots per unit: the most warps whose ranges can meet one unit
-  const int64_t len_min = p.total / nwarps;
-  p.maxseg = len_min == 0 ? int(p.NI < nwarps ? p.NI : nwarps) + 1 : int((p.NI + len_min - 1) / len_min + 1);
+  p.nchunks = nwarps * PKV_ACHUNKS < p.total ? nwarps * PKV_ACHUNKS : (p.total > 0 ? p.total : 1);
+  // slots per unit: the most chunks whose ranges can meet one unit
+  const int64_t len_min = p.total / p.nchunks;
+  p.maxseg = len_min == 0 ? int(p.NI < p.nchunks ? p.NI : p.nchunks) + 1 : int((p.NI + len_min - 1) / len_min + 1);
   return p;
 }
 
 }  // namespace
 
-// Scratch: the arrival counters [U] (zeroed by every call), then the partials
-// [U][maxseg][G][kPartA] f32.
+// Scratch: 16 reserved bytes, the inline-merge arrival counters [U], then
+// the partials [U][maxseg][G][kPartA] f32.
 int64_t pkv_fast_attention1_scratch(const pkv_layer_t* L, int nblocks, int G) {
   const AttnPlan p = attn_plan(L, nblocks, G);
   const int64_t U = int64_t(L->batch) * L->heads;
-  return (U + 3) / 4 * 16 + U * p.maxseg * G * kPartA * 4;
+  return 16 + (U + 3) / 4 * 16 + U * p.maxseg * G * kPartA * 4;
 }
 
 int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G, float* out, void* scratch,
                         cudaStream_t s) {
   const AttnPlan p = attn_plan(L, nblocks, G);
   const int64_t U = int64_t(L->batch) * L->heads;
-  int* cnt = (int*)scratch;
-  float* part = (float*)((uint8_t*)scratch + (U + 3) / 4 * 16);
-  cudaError_t e = cudaMemsetAsync(cnt, 0, U * sizeof(int), s);
-  if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): counters");
+  static const bool inline_merge = [] {
+    const char* e = getenv("PKV_ATTN_INLINE_MERGE");
+    return e && e[0] == '1';
+  }();
+  int* cnt = inline_merge ? (int*)((uint8_t*)scratch + 16) : nullptr;
+  float* part = (float*)((uint8_t*)scratch + 16 + (U + 3) / 4 * 16);
+  if (inline_merge) {
+    cudaError_t e = cudaMemsetAsync(cnt, 0, U * sizeof(int), s);
+    if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): counters");
+  }
   if (G <= 4)
-    attn_fused_kernel<1><<<p.grid, kWA * 32, a_smem_bytes(), s>>>(*L, q, G, p.NB, p.NI, p.total, part, p.maxseg, cnt,
-                                                                  out);
+    attn_fused_kernel<1><<<p.grid, kWA * 32, a_smem_bytes(), s>>>(*L, q, G, p.NB, p.NI, p.total, p.nchunks, part,
+                                                                  p.maxseg, cnt, out);
   else
-    attn_fused_kernel<2><<<p.grid, kWA * 32, a_smem_bytes(), s>>>(*L, q, G, p.NB, p.NI, p.total, part, p.maxseg, cnt,
-                                                                  out);
+    attn_fused_kernel<2><<<p.grid, kWA * 32, a_smem_bytes(), s>>>(*L, q, G, p.NB, p.NI, p.total, p.nchunks, part,
+                                                                  p.maxseg, cnt, out);
+  if (!inline_merge && !PKV_ADIAG) {
+    const int ug = int(U) * G;
+    attn_merge_kernel<<<ug < 148 * 2 ? ug : 148 * 2, 128 * kMQ, 0, s>>>(*L, G, p.NI, p.total, p.nchunks, part,
+                                                                        p.maxseg, out);
+  }
   return pkv_cuda_status(cudaGetLastError(), "pkv_attention_decode(single pass)");
 }

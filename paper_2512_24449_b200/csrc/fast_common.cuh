@@ -439,6 +439,7 @@ struct Feed {
   int64_t offl;
   int lenl;          // -1: no block (past nblk)
   int NI = 0;        // range items per unit (0: NB)
+  int base = 0;      // feed index of the current range's first item (ranges fed one after another)
 
   __device__ __forceinline__ void init(uint8_t* smem, int lane) {
     ring = smem;
@@ -461,7 +462,7 @@ struct Feed {
   // (re)load the directory entries of the warp's blocks kk .. kk+31
   __device__ __forceinline__ void load_dir(const pkv_layer_t& L, int kind, int NB, const Range& rg, int kk, int lane) {
     k0 = kk;
-    const int it = kk + lane;
+    const int it = kk + lane - base;
     const int64_t gb = rg.b0 + (PAIRED ? (it >> 1) : it);
     const int kd = PAIRED ? (it & 1) : kind;
     const int ni = NI ? NI : NB;
@@ -636,6 +637,104 @@ __device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G,
       const uint32_t hi = __byte_perm(x[2], x[3], 0x0062u);
       F.s[jj][r] = __byte_perm(lo, hi, 0x5410u);
     }
+}
+
+// Query operand with TWO signed byte digits (one u8 x s8 IMMA per k-step and
+// tile, half the tensor-core work of QFrag's unsigned pair + signed third
+// digit; the legacy mma.sync IMMA issues ~0.45 per SM-cycle on B200,
+// tools/probe/mma_rate_probe.cu): x = rint(q * f_head) with f_head = 32000 /
+// max|q_head| (|x| <= 32000), x = d0 + 256 d1, d0 = the sign-extended low byte,
+// d1 = (x - d0) / 256 in [-125, 125].  Column gi of tile nu = (head 4nu + gi/2,
+// digit gi&1).  Per element the rounding is <= max|q| / 64000; the int32 tile
+// sums are exact (|sum| <= 128 * 255 * 32000 < 2^31).
+#ifndef PKV_Q2
+#define PKV_Q2 1
+#endif
+// the K tile products of one k-step and the score value of tile nu, rows gi (half 0) / gi + 8 (half 1)
+template <int NU, class QF>
+__device__ __forceinline__ void k_mma(int (&accU)[NU][4], int (&accS)[4], const uint32_t (&a)[4], const QF& Q, int jj);
+template <int NU>
+struct QFrag2;
+template <int NU>
+__device__ __forceinline__ void k_mma(int (&accU)[NU][4], int (&accS)[4], const uint32_t (&a)[4], const QFrag<NU>& Q,
+                                      int jj) {
+#pragma unroll
+  for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, Q.u[nu][jj][0], Q.u[nu][jj][1]);
+  imma_us(accS, a, Q.s[jj][0], Q.s[jj][1]);
+}
+template <int NU>
+__device__ __forceinline__ void k_mma(int (&accU)[NU][4], int (&)[4], const uint32_t (&a)[4], const QFrag2<NU>& Q,
+                                      int jj) {
+#pragma unroll
+  for (int nu = 0; nu < NU; ++nu) imma_us(accU[nu], a, Q.u[nu][jj][0], Q.u[nu][jj][1]);
+}
+template <int NU>
+__device__ __forceinline__ float k_val(const int (&accU)[NU][4], const int (&accS)[4], const QFrag<NU>&, int nu,
+                                       int half) {
+  // digit sums: d0 + 256*d1 <= 128*255*65535 < 2^31 is exact in int32
+  return fmaf(65536.f, float(accS[2 * half + nu]), float(accU[nu][2 * half] + 256 * accU[nu][2 * half + 1]));
+}
+template <int NU>
+__device__ __forceinline__ float k_val(const int (&accU)[NU][4], const int (&)[4], const QFrag2<NU>&, int nu, int half) {
+  return float(accU[nu][2 * half] + 256 * accU[nu][2 * half + 1]);
+}
+template <int NU>
+struct QFrag2 {
+  uint32_t u[NU][4][2];
+  float qs[2], inv[2];  // sum(q) and 1/f of heads tq and tq+4
+};
+template <int NU>
+__device__ __forceinline__ void build_qfrag(const float* __restrict__ qu, int G, int lane, QFrag2<NU>& F) {
+  const int gi = lane >> 2, tq = lane & 3;
+  constexpr int GH = 4 * NU;
+  float mx[8], sm[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) mx[g] = sm[g] = 0.f;
+#pragma unroll
+  for (int g = 0; g < GH; ++g) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g < G) v = *(const float4*)(qu + g * kD + 4 * lane);
+    mx[g] = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+    sm[g] = (v.x + v.y) + (v.z + v.w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int g = 0; g < GH; ++g) {
+      mx[g] = fmaxf(mx[g], __shfl_xor_sync(PKV_FULL, mx[g], o));
+      sm[g] += __shfl_xor_sync(PKV_FULL, sm[g], o);
+    }
+  float f[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) f[g] = mx[g] > 1e-30f ? 32000.f / mx[g] : 1.f;
+  F.qs[0] = sel8(sm, tq);
+  F.qs[1] = sel8(sm, tq + 4);
+  F.inv[0] = 1.f / sel8(f, tq);
+  F.inv[1] = 1.f / sel8(f, tq + 4);
+  const bool hi_digit = (gi & 1) != 0;
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int nu = 0; nu < NU; ++nu) {
+        const int g = 4 * nu + (gi >> 1);
+        uint32_t d[4] = {0u, 0u, 0u, 0u};
+        if (g < G) {
+          const float4 v = *(const float4*)(qu + g * kD + 32 * jj + 16 * r + 4 * tq);
+          const float fg = sel8(f, g);
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int x = __float2int_rn(vv[e] * fg);
+            const int d0 = int(int8_t(x & 0xff));
+            d[e] = uint32_t(hi_digit ? (x - d0) >> 8 : x);
+          }
+        }
+        const uint32_t lo = __byte_perm(d[0], d[1], 0x0040u);
+        const uint32_t hi = __byte_perm(d[2], d[3], 0x0040u);
+        F.u[nu][jj][r] = __byte_perm(lo, hi, 0x5410u);
+      }
 }
 
 }  // namespace

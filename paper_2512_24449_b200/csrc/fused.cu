@@ -430,7 +430,8 @@ extern "C" int64_t pkv_attention_scratch_bytes(const pkv_layer_t* L, int32_t nbl
   int G = 0;
   if (fused_args(L, nblocks, q_heads, &G)) return -1;
   if (!pkv_fast_supported(L, G, 4)) return 0;
-  const int64_t a3 = pkv_fast_attention_scratch(L, nblocks, G), a1 = pkv_fast_attention1_scratch(L, nblocks, G);
+  // the three-launch path uses the bytes after the single pass's 16-byte work counter
+  const int64_t a3 = 16 + pkv_fast_attention_scratch(L, nblocks, G), a1 = pkv_fast_attention1_scratch(L, nblocks, G);
   return a3 > a1 ? a3 : a1;
 }
 
@@ -458,10 +459,11 @@ extern "C" int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const
                   (long long)nblocks * L->block);
     return PKV_E_SHAPE;
   }
-  if (scratch_bytes < pkv_fast_attention_scratch(L, nblocks, G)) {
+  if (scratch_bytes < 16 + pkv_fast_attention_scratch(L, nblocks, G)) {
     pkv_set_error("attention scratch too small");
     return PKV_E_ARG;
   }
   pkv_note_path(PKV_PATH_FAST);
-  return pkv_fast_attention(L, nblocks, q, G, scores, score_stride, out, (float*)scratch, (cudaStream_t)stream);
+  return pkv_fast_attention(L, nblocks, q, G, scores, score_stride, out, (float*)((uint8_t*)scratch + 16),
+                            (cudaStream_t)stream);
 }

@@ -119,7 +119,11 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   const int64_t nwarps = int64_t(gridDim.x) * kWK, wid = int64_t(blockIdx.x) * kWK + warp;
   const Range rg = warp_range(total, wid, nwarps);
   const int nk = int(rg.b1 - rg.b0);
+#if PKV_Q2
+  QFrag2<NU> Q;
+#else
   QFrag<NU> Q;
+#endif
   int cur_u = -1;
   float* sbase = scores;
   float kmx0 = -INFINITY, kmx1 = -INFINITY;  // running max of this lane's scores (heads tq, tq + 4)
@@ -259,24 +263,22 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
             for (int jj = 0; jj < 4; ++jj) {
               uint32_t a[4];
               ldsm_t(a, (jj < 2 ? a0 : a1) + 512u * (jj & 1));
-  #pragma unroll
-              for (int nu = 0; nu < NU; ++nu) imma_uu(accU[nu], a, Q.u[nu][jj][0], Q.u[nu][jj][1]);
-              imma_us(accS, a, Q.s[jj][0], Q.s[jj][1]);
+                k_mma<NU>(accU, accS, a, Q, jj);
             }
             const float sA = h2f(prm[g][0] & 0xffff), zA = h2f(prm[g][0] >> 16);
             const float sB = h2f(prm[g][1] & 0xffff), zB = h2f(prm[g][1] >> 16);
             // digit sums: d0 + 256*d1 <= 128*255*65535 < 2^31 is exact in int32
             if (tq < G) {
-              const float vA = fmaf(65536.f, float(accS[0]), float(accU[0][0] + 256 * accU[0][1]));
-              const float vB = fmaf(65536.f, float(accS[2]), float(accU[0][2] + 256 * accU[0][3]));
+              const float vA = k_val<NU>(accU, accS, Q, 0, 0);
+              const float vB = k_val<NU>(accU, accS, Q, 0, 1);
               const float scA = fmaf(sA, vA * Q.inv[0], zA * Q.qs[0]), scB = fmaf(sB, vB * Q.inv[0], zB * Q.qs[0]);
               p0[16 * g] = scA;
               p0[16 * g + 8] = scB;
               if (ST) kmx0 = fmaxf(kmx0, fmaxf(scA, scB));
             }
             if (NU == 2 && tq + 4 < G) {
-              const float vA = fmaf(65536.f, float(accS[1]), float(accU[NU - 1][0] + 256 * accU[NU - 1][1]));
-              const float vB = fmaf(65536.f, float(accS[3]), float(accU[NU - 1][2] + 256 * accU[NU - 1][3]));
+              const float vA = k_val<NU>(accU, accS, Q, NU - 1, 0);
+              const float vB = k_val<NU>(accU, accS, Q, NU - 1, 1);
               const float scA = fmaf(sA, vA * Q.inv[1], zA * Q.qs[1]), scB = fmaf(sB, vB * Q.inv[1], zB * Q.qs[1]);
               p1[16 * g] = scA;
               p1[16 * g + 8] = scB;

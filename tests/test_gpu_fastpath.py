@@ -190,7 +190,7 @@ def test_smoke_entry_runs_fast_kernels():
     import __graft_entry__ as ge
     N, _, _, _ = _mods()
     ge.smoke()
-    assert N.last_path() == N.PATH_FAST
+    assert N.last_path() == N.PATH_SINGLE  # smoke() asserts PATH_FAST after its K and V calls
 
 
 def test_graphed_decode_loop_device_flush():

@@ -45,7 +45,7 @@ def _oracle_attention(ref, h, q):
 
 
 def _single(N, A, st, q, **kw):
-    out = A(st, 0, q, **kw)
+    out = A(st, 0, q, single_pass=True, **kw)
     assert N.last_path() == N.PATH_SINGLE, "attention left the single-pass kernel"
     return out
 

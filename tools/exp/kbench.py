@@ -24,7 +24,8 @@ w = torch.softmax(torch.randn((B, Hq, L), device="cuda"), -1)
 out = torch.empty((B, Hq, D), device="cuda")
 fns = {"k": lambda: F.fused_k_scores_batched(st, 0, q, out=scores),
        "v": lambda: F.fused_v_output_batched(st, 0, w, out=out),
-       "a": lambda: attention_decode_batched(st, 0, q, scores=scores, out=out)}
+       "a": lambda: attention_decode_batched(st, 0, q, scores=scores, out=out, single_pass=False),
+       "s": lambda: attention_decode_batched(st, 0, q, out=out, single_pass=True)}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name in a.which:
     fn = fns[name]
@@ -46,6 +47,6 @@ for name in a.which:
         e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3 / 16)
     t = statistics.median(ts)
-    extra = {"k": B * Hq * L * 4 + B * Hq * D * 4, "v": B * Hq * L * 4 + B * Hq * D * 4, "a": 0}[name]
+    extra = {"k": B * Hq * L * 4 + B * Hq * D * 4, "v": B * Hq * L * 4 + B * Hq * D * 4, "a": 0, "s": 0}[name]
     pb = (phys[0] if name == "k" else phys[1] if name == "v" else phys[0] + phys[1]) + extra
-    print(f"{a.cfg} {name}: {t:.2f} us  phys {pb / t / 1e3:.0f} GB/s  frac {pb / t / 1e3 / 6532.9:.3f}  equiv {B*Hkv*L*D*2*(2 if name=='a' else 1)/t/1e3:.0f} GB/s")
+    print(f"{a.cfg} {name}: {t:.2f} us  phys {pb / t / 1e3:.0f} GB/s  frac {pb / t / 1e3 / 6532.9:.3f}  equiv {B*Hkv*L*D*2*(2 if name in 'as' else 1)/t/1e3:.0f} GB/s")
