@@ -178,6 +178,13 @@ int pkv_repack_plan(const uint16_t* codes, int32_t nsets, int32_t batch, int32_t
 int64_t pkv_flush_scratch_bytes(const pkv_layer_t* L);
 int pkv_flush_staged(const pkv_layer_t* L, float rel_k, float rel_v, void* scratch, int64_t scratch_bytes,
                      void* stream);
+/* pkv_stage_token + pkv_flush_staged in ONE launch (append_token for the
+ * decode loop): each (sequence, kind, head) warp stages its
+ * token at the device residue count, and a block-set the token completes is
+ * compressed at once -- attention after it sees the compressed block, as the
+ * reference's append_token does.  Scratch: pkv_flush_scratch_bytes.        */
+int pkv_append_flush(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new, float rel_k, float rel_v,
+                     void* scratch, int64_t scratch_bytes, void* stream);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:
  * [B][ntok][H][D] fp16.  `staged` = tokens already staged per sequence
  * (host mirror of nres, < block); `nblocks_before` = blocks per sequence

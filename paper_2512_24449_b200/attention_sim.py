@@ -17,7 +17,8 @@ from .kv_store import CompressedStore, ctypes_ref
 
 
 def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride: int = 0, scores=None,
-                             out=None, nblocks: int = None, single_pass: bool = None) -> torch.Tensor:
+                             out=None, nblocks: int = None, single_pass: bool = None,
+                             prescaled: bool = False) -> torch.Tensor:
     """q [B, Hq, D] -> out [B, Hq, D].
 
     The 1/sqrt(d) scale is applied to the (small) query instead of the
@@ -42,7 +43,9 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     single_pass_preferred), where it measured faster (config C: 622 vs 482
     tokens/s); the three-launch path at long contexts, where its two
     kernels issue faster (config B 131 vs 140 us)."""
-    q = _as_f32(q, store.device) * (1.0 / math.sqrt(store.head_dim))
+    q = _as_f32(q, store.device)
+    if not prescaled:  # prescaled: the caller already multiplied q by 1/sqrt(d)
+        q = q * (1.0 / math.sqrt(store.head_dim))
     ls = store[layer]
     B, H, D = store.batch, store.heads, store.head_dim
     if q.dim() != 3 or q.shape[0] != B or q.shape[2] != D or q.shape[1] % H:
@@ -279,6 +282,11 @@ class GraphedDecodeLoop:
     (every headroom * 64 tokens) or a buffer moves.  Default format, repack
     "none" (GraphedDecodeStep serves the others).
 
+    Default (fused_append): the token is staged and a completed block
+    compressed in ONE launch per layer (pkv_append_flush) instead of two
+    (pkv_stage_token, pkv_flush_staged); fused_append = False keeps them
+    separate.
+
     step(k, v, q): k / v [layers, B, 1, H, D] (or [layers, B, H, D]) fp16,
     q [layers, B, Hq, D] f32 -> out [layers, B, Hq, D] (a static buffer,
     overwritten by the next step).  inputs() returns the static input buffers;
@@ -286,6 +294,7 @@ class GraphedDecodeLoop:
     skips the copies."""
 
     single_pass = None  # None: single_pass_preferred; True / False force a path
+    fused_append = True
 
     def __init__(self, store: CompressedStore, q_heads: int, layers=None, headroom: int = 16):
         self.store = store
@@ -340,24 +349,33 @@ class GraphedDecodeLoop:
             if ls.a_scratch.numel() < need:
                 ls.a_scratch = torch.zeros(need, dtype=torch.uint8, device=o.device)
             stride = (self._cap[i] * o.block + o.buffer + 3) // 4 * 4
-            if self._scores[i] is None or self._scores[i].shape[-1] < stride:
+            sp = self.single_pass if self.single_pass is not None else single_pass_preferred(o, self._cap[i])
+            if not sp and (self._scores[i] is None or self._scores[i].shape[-1] < stride):
                 self._scores[i] = torch.empty((B, Hq, stride), dtype=torch.float32, device=o.device)
+        if getattr(self, "_qs", None) is None or self._qs.shape != self.q.shape:
+            self._qs = torch.empty_like(self.q)
 
     def _record(self, with_append: bool):
         o = self.store
         lib = N.lib()
+        torch.mul(self.q, 1.0 / math.sqrt(o.head_dim), out=self._qs)  # every layer's query in one launch
         for i, l in enumerate(self.layers):
             ls = o[l]
             L = ctypes_ref(ls.struct())
-            if with_append:
-                N.check(lib.pkv_stage_token(L, N.ptr(self.k[i]), N.ptr(self.v[i]), N.stream()), "stage_token")
-            N.check(lib.pkv_flush_staged(L, float(o.rel_scale_k), float(o.rel_scale_v), N.ptr(self._flush_scr[i]),
-                                         int(self._flush_scr[i].numel()), N.stream()), "flush_staged")
+            if with_append and self.fused_append:
+                N.check(lib.pkv_append_flush(L, N.ptr(self.k[i]), N.ptr(self.v[i]), float(o.rel_scale_k),
+                                             float(o.rel_scale_v), N.ptr(self._flush_scr[i]),
+                                             int(self._flush_scr[i].numel()), N.stream()), "append_flush")
+            else:
+                if with_append:
+                    N.check(lib.pkv_stage_token(L, N.ptr(self.k[i]), N.ptr(self.v[i]), N.stream()), "stage_token")
+                N.check(lib.pkv_flush_staged(L, float(o.rel_scale_k), float(o.rel_scale_v), N.ptr(self._flush_scr[i]),
+                                             int(self._flush_scr[i].numel()), N.stream()), "flush_staged")
             sp = self.single_pass
             if sp is None:
                 sp = single_pass_preferred(o, self._cap[i])
-            attention_decode_batched(o, l, self.q[i], scores=self._scores[i], out=self.out[i], nblocks=self._cap[i],
-                                     single_pass=sp)
+            attention_decode_batched(o, l, self._qs[i], scores=self._scores[i], out=self.out[i], nblocks=self._cap[i],
+                                     single_pass=sp, prescaled=True)
 
     def _capture(self):
         dev = torch.device(self.store.device)

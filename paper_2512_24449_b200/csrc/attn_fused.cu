@@ -799,7 +799,7 @@ int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G
   }();
   int* cnt = inline_merge ? (int*)((uint8_t*)scratch + 16) : nullptr;
   float* part = (float*)((uint8_t*)scratch + 16 + (U + 3) / 4 * 16);
-  if (inline_merge) {
+  if (cnt) {
     cudaError_t e = cudaMemsetAsync(cnt, 0, U * sizeof(int), s);
     if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): counters");
   }
@@ -809,7 +809,7 @@ int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G
   else
     attn_fused_kernel<2><<<p.grid, kWA * 32, a_smem_bytes(), s>>>(*L, q, G, p.NB, p.NI, p.total, p.nchunks, part,
                                                                   p.maxseg, cnt, out);
-  if (!inline_merge && !PKV_ADIAG) {
+  if (!cnt && !PKV_ADIAG) {
     const int ug = int(U) * G;
     attn_merge_kernel<<<ug < 148 * 2 ? ug : 148 * 2, 128 * kMQ, 0, s>>>(*L, G, p.NI, p.total, p.nchunks, part,
                                                                         p.maxseg, out);
