@@ -150,9 +150,22 @@ def naive_v_output(store: CompressedStore, layer: int, head: int, w) -> torch.Te
     return _as_f32(w, store.device).double() @ V
 
 
+REPORT_FIELDS = ("kind", "mode", "tokens", "bytes_logical", "bytes_physical", "wall_ns", "gbps", "peak_alloc")
+
+
 def bench_throughput(store: CompressedStore, layer: int, mode: str = "fused", reps: int = 10, q_heads=None):
     """SPEC.md:472-480 ThroughputReport rows {kind, mode, tokens, bytes_logical,
-    bytes_physical, wall_ns, gbps, peak_alloc}, CUDA-event timed."""
+    bytes_physical, wall_ns, gbps, peak_alloc}, CUDA-event timed.
+
+    gbps is over the uncompressed-equivalent bytes.  peak_alloc
+    is the transient device allocation of one call beyond the tensor it
+    returns (fused: nothing context-sized -- the split-L scratch is cached in
+    the store after a warm-up call; naive: the dense [B*H, L, D] matrix),
+    measured with torch's allocator counters around the call."""
+    if mode not in ("fused", "naive"):
+        raise ValueError("mode must be 'fused' or 'naive'")
+    if reps < 1:
+        raise ValueError("reps >= 1")
     ls = store[layer]
     B, H, D = store.batch, store.heads, store.head_dim
     Hq = q_heads or H
@@ -165,10 +178,14 @@ def bench_throughput(store: CompressedStore, layer: int, mode: str = "fused", re
                      (1, lambda: fused_v_output_batched(store, layer, w))):
         if mode == "naive":
             fn = (lambda kind=kind: decode_layer(store, layer, kind))
+        fn()  # warm-up: scratch cached in the store, modules loaded
         torch.cuda.synchronize()
         base = torch.cuda.memory_allocated()
         torch.cuda.reset_peak_memory_stats()
-        fn()
+        r = fn()
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated() - base - r.numel() * r.element_size()
+        del r
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
@@ -179,6 +196,23 @@ def bench_throughput(store: CompressedStore, layer: int, mode: str = "fused", re
         logical = B * H * L * D * 2
         phys = int(ln[kind].astype(np.int64).sum()) + B * H * ls.nres_h * D * 2
         rows.append({"kind": "K" if kind == 0 else "V", "mode": mode, "tokens": L, "bytes_logical": logical,
-                     "bytes_physical": phys, "wall_ns": t, "gbps": logical / t,
-                     "peak_alloc": torch.cuda.max_memory_allocated() - base})
+                     "bytes_physical": phys, "wall_ns": t, "gbps": logical / t, "peak_alloc": max(0, int(peak))})
     return rows
+
+
+def report_rows(rows, fmt: str = "json") -> str:
+    """ThroughputReport serialised as JSON lines or CSV rows, the
+    fields in REPORT_FIELDS order."""
+    import csv
+    import io
+    import json
+    if fmt == "json":
+        return "\n".join(json.dumps({k: r[k] for k in REPORT_FIELDS}) for r in rows) + "\n"
+    if fmt == "csv":
+        buf = io.StringIO()
+        wr = csv.DictWriter(buf, fieldnames=REPORT_FIELDS, lineterminator="\n")
+        wr.writeheader()
+        for r in rows:
+            wr.writerow({k: r[k] for k in REPORT_FIELDS})
+        return buf.getvalue()
+    raise ValueError("fmt must be 'json' or 'csv'")

@@ -69,15 +69,23 @@ def gauss_outlier(shape, head_dim_axis: int = -1, n_outlier: int = 4, amp: float
     D = shape[head_dim_axis]
     H = shape[heads_axis]
     if n_outlier:
+        # per kv head a fixed set of channels (the CPU generator's draws, head by
+        # head), applied in one broadcast op instead of a launch chain per head
         gc = torch.Generator(device="cpu")
         gc.manual_seed(seed + 1)
+        mask = torch.zeros((H, D), dtype=torch.bool)
+        sgn = torch.zeros((H, D), dtype=torch.float32)
         for h in range(H):
             ch = torch.randperm(D, generator=gc)[:n_outlier]
             sign = (torch.randint(0, 2, (n_outlier,), generator=gc) * 2 - 1).float()
-            idx = [slice(None)] * len(shape)
-            idx[heads_axis] = h
-            sub = x[tuple(idx)]                      # (..., D) view
-            sub[..., ch.to(device)] = sign.to(device) * amp + sigma * sub[..., ch.to(device)]
+            mask[h, ch] = True
+            sgn[h, ch] = sign
+        bshape = [1] * len(shape)
+        bshape[heads_axis] = H
+        bshape[head_dim_axis] = D
+        mask = mask.view(bshape).to(device)
+        sgn = sgn.view(bshape).to(device)
+        x = torch.where(mask, sgn * amp + sigma * x, x)
     return x.to(torch.float16)
 
 
