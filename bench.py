@@ -756,6 +756,8 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks([a0.elapsed_time(a1) / K], world)[0]
     e2e_value = world * 2 * logical_kind / (e2e_ms * 1e-3) / 1e9
+    from paper_2512_24449_b200.attention_sim import single_pass_preferred
+    e2e_attn = "single-pass" if single_pass_preferred(st, st[0].nblk_h) else "three-launch"
 
     peak, peak_src = load_peaks()
     dom = "k" if k_ms >= v_ms else "v"
@@ -811,13 +813,13 @@ def main():
                 "single_pass_gbs_equiv": round(2 * kind_layer / (attn_us["single"] * 1e-6) / 1e9, 1),
                 "algorithmic_bytes_per_launch": int(alg_attn),
                 "per": "one layer: softmax(q K^T / sqrt(d)) V over this rank's units, graph-replayed; single "
-                       "pass = attn_fused_kernel (+ counter memset), three launch = fused K + fused V + finalize"},
+                       "pass = attn_fused_kernel + attn_merge_kernel, three launch = fused K + fused V + finalize"},
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": layers * Bl * Hql * D * 4,
                     "d2h_bytes_per_step": layers * world * Bl * Hql * D * 4,
                     "path": "sharding.ShardedDecoder.step (public API) per layer on the pinned host q shard: H2D "
-                            "straight into the graph's input buffer, one CUDA-graph replay of the single-pass "
-                            "decode attention (attention_sim.GraphedAttention -> attn_fused_kernel), all-gather of "
-                            "per-head outputs, D2H out",
+                            "straight into the graph's input buffer, one CUDA-graph replay of the decode attention "
+                            f"(attention_sim.GraphedAttention, {e2e_attn} path per single_pass_preferred), all-gather "
+                            "of per-head outputs, D2H out",
                     "ms_per_step": round(e2e_ms, 5)},
             "memory": mem,
             # scaling with and without the all-gather -- the same

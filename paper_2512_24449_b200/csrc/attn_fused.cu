@@ -48,6 +48,9 @@ constexpr int kResRows = 32;          // residue rows per range item
 #ifndef PKV_ADIAG  // diagnostics build: per-warp cycle counters into `out` (results wrong)
 #define PKV_ADIAG 0
 #endif
+#ifndef PKV_AMINB2  // the same for G <= 8 (NG = 2)
+#define PKV_AMINB2 4
+#endif
 #ifndef PKV_AREGC  // pack width constants in registers (1) or from the shared table (0)
 #define PKV_AREGC 0
 #endif
@@ -66,7 +69,7 @@ __device__ __forceinline__ float ldcg_f(const float* p) { return __ldcg(p); }
 __host__ __device__ __forceinline__ int res_items(int buffer) { return (buffer + kResRows - 1) / kResRows; }
 
 template <int NG>  // NG = 1: G <= 4 (one digit tile / n-tile), 2: G <= 8
-__global__ void __launch_bounds__(kWA * 32, PKV_AMINB)
+__global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
     attn_fused_kernel(pkv_layer_t L, const float* __restrict__ q, int G, int NB, int NI, int64_t total,
                       int64_t nchunks, float* __restrict__ part, int maxseg,
                       int* __restrict__ cnt, float* __restrict__ out) {

@@ -436,6 +436,9 @@ constexpr int kWV = 4;
 #ifndef PKV_VMINB  // V: CTAs per SM the register allocation must allow
 #define PKV_VMINB 4
 #endif
+#ifndef PKV_VMINB2  // the same for the G <= 8 instantiation (two n-tiles)
+#define PKV_VMINB2 4
+#endif
 #ifndef PKV_RBV  // V ring: 11 KB still fits 4 register-bound CTAs per SM (measured ~2% over 10 KB)
 #define PKV_RBV 11264
 #endif
@@ -448,7 +451,7 @@ constexpr size_t kWarpSmemV = (2048 + FeedV::bytes() + 127) / 128 * 128;
 // the K launch's statistics (kmax over its kslots warp slots, kres), so no
 // rescaling is ever needed, and each partial slot also carries l = sum p.
 template <int NT, bool SM>  // NT: n-tiles, 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kWV * 32, PKV_VMINB) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
+__global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fused_v_fast_kernel(pkv_layer_t L, const float* __restrict__ w, int G,
                                                                  int64_t wstride, float* __restrict__ part, int NB,
                                                                  int64_t total, int maxseg,
                                                                  float* __restrict__ vscr,

@@ -126,6 +126,44 @@ def full(tag):
     json.dump(js, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
 
 
+def single(tag):
+    """profiles/<tag>_single_pass.md: the single-pass attention kernel's ncu
+    summary and the config C decode-step launch list (per layer)."""
+    lines = [f"# Single-pass decode attention and the decode loop ({tag})", ""]
+    rep = os.path.join(OUT, "prof_single.ncu-rep")
+    if os.path.exists(rep):
+        rows = ncu_csv(["-i", rep, "--page", "raw", "--csv"])
+        h = rows[0]
+        want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+                "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+                "launch__registers_per_thread", "smsp__cycles_active.avg", "sm__cycles_elapsed.avg"]
+        stalls = [i for i, x in enumerate(h) if "smsp__average_warps_issue_stalled" in x and "per_issue_active" in x]
+        lines += ["`ncu --set full` of attn_fused_kernel<1> on config B (tools/exp/kbench.py s)", ""]
+        for r in rows[2:]:
+            lines += [f"## `{short(r[h.index('Kernel Name')])}`", "", "| metric | value |", "|---|---|"]
+            lines += [f"| {m} | {r[h.index(m)]} |" for m in want if m in h]
+            top = sorted(((float(r[i] or 0), h[i]) for i in stalls), reverse=True)[:7]
+            lines += ["", "Top warp stall reasons (warps per issue): " + ", ".join(
+                f"{n.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')} {v:.2f}"
+                for v, n in top), ""]
+    path = os.path.join(OUT, "launches_C.csv")
+    if os.path.exists(path):
+        allrows = [r for r in csv.reader(open(path)) if r]
+        hdr = next(r for r in allrows if r[0] == "ID")
+        ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+        ks = [(short(r[ik]), float(r[iv].replace(",", ""))) for r in allrows if r[0].isdigit()]
+        tail = ks[-40 * 10 * 3:]
+        per = defaultdict(list)
+        for k, v in tail:
+            per[k].append(v)
+        lines += ["## Config C decode step: launch list (steady state, cold-cache, serialised)", "",
+                  "`ncu --metrics gpu__time_duration.sum python bench.py --config C --stream-steps 200` (the last "
+                  "launches: 40 layers per step)", "", "| kernel | launches | mean us |", "|---|---|---|"]
+        for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+            lines.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1e3:.2f} |")
+    open(os.path.join(PROF, f"{tag}_single_pass.md"), "w").write("\n".join(lines) + "\n")
+
+
 def compressor(tag):
     """profiles/<tag>_compressor.md: prefill launch list (time, DRAM bytes) and
     the full-set summary of the warp-per-block compressor kernels."""
@@ -172,5 +210,6 @@ if __name__ == "__main__":
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
     full(tag)
+    single(tag)
     compressor(tag)
     print(open(os.path.join(PROF, "ncu_traffic.json")).read())
