@@ -545,14 +545,15 @@ def run_streaming(args, rank, world, local, backend):
                        "l2": "per-step working set (40 layers of compressed K+V) exceeds the 126 MB L2"},
             "tokens_per_s": round(tok_s, 1), "us_per_token": round(ms * 1e3 / timed, 2),
             "step": ("GraphedDecodeLoop: one CUDA-graph replay per token: for each of the 40 layers "
-                     "pkv_stage_token + pkv_flush_staged (device-side block completion) + pkv_attention_decode; "
+                     "pkv_append_flush (token staged + device-side block completion, one launch) + "
+                     "pkv_attention_decode (single pass: attn_fused_kernel + attn_merge_kernel); "
                      f"re-captures {loop.captures} (every {loop.headroom * 64} tokens)"),
             "e2e": {"value": round(world * e2e_logical / (e2e_ms * 1e-3) / 1e9, 2), "unit": UNIT,
                     "h2d_bytes_per_step": Ly * B * (2 * H * D * 2 + Hq * D * 4),
                     "d2h_bytes_per_step": Ly * B * Hq * D * 4,
                     "tokens_per_s": round(world * 1e3 / e2e_ms, 1), "ms_per_step": round(e2e_ms, 5),
                     "path": "GraphedDecodeLoop.step from pinned host k/v/q, output copied back each step"},
-            "gpu_launches": timed * Ly * 6, "clocks": sampler.summary(),
+            "gpu_launches": timed * (Ly * 3 + 1), "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
 

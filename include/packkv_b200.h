@@ -174,7 +174,10 @@ int pkv_repack_plan(const uint16_t* codes, int32_t nsets, int32_t batch, int32_t
  * pkv_stage_token + pkv_flush_staged + pkv_attention_decode (with nblocks
  * headroom, blocks past nblk[b] are skipped) is one CUDA graph for every
  * step.  The arena must have room (PKV_FLAG_CAPACITY otherwise).  Scratch:
- * pkv_flush_scratch_bytes(L) (look-back words, zeroed by the call).       */
+ * pkv_flush_scratch_bytes(L) (look-back words, ticket and epoch): zero it
+ * once before the first call with it (cudaMemset); every call leaves it ready
+ * for the next -- the words are tagged with a per-call epoch, so no memset
+ * sits in the decode graph.  Calls sharing a scratch must be stream-ordered. */
 int64_t pkv_flush_scratch_bytes(const pkv_layer_t* L);
 int pkv_flush_staged(const pkv_layer_t* L, float rel_k, float rel_v, void* scratch, int64_t scratch_bytes,
                      void* stream);
@@ -182,7 +185,8 @@ int pkv_flush_staged(const pkv_layer_t* L, float rel_k, float rel_v, void* scrat
  * decode loop): each (sequence, kind, head) warp stages its
  * token at the device residue count, and a block-set the token completes is
  * compressed at once -- attention after it sees the compressed block, as the
- * reference's append_token does.  Scratch: pkv_flush_scratch_bytes.        */
+ * reference's append_token does.  Scratch: pkv_flush_scratch_bytes, zeroed
+ * once before first use (as for pkv_flush_staged).                         */
 int pkv_append_flush(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new, float rel_k, float rel_v,
                      void* scratch, int64_t scratch_bytes, void* stream);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:

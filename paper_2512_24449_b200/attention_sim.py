@@ -344,7 +344,7 @@ class GraphedDecodeLoop:
             L = ls.struct()
             fb = int(lib.pkv_flush_scratch_bytes(ctypes_ref(L)))
             if self._flush_scr[i] is None or self._flush_scr[i].numel() < fb:
-                self._flush_scr[i] = torch.empty(fb, dtype=torch.uint8, device=o.device)
+                self._flush_scr[i] = torch.zeros(fb, dtype=torch.uint8, device=o.device)  # zero before first use
             need = int(lib.pkv_attention_scratch_bytes(ctypes_ref(L), self._cap[i], Hq))
             if ls.a_scratch.numel() < need:
                 ls.a_scratch = torch.zeros(need, dtype=torch.uint8, device=o.device)

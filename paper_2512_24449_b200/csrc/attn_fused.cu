@@ -48,14 +48,14 @@ constexpr int kResRows = 32;          // residue rows per range item
 #ifndef PKV_ADIAG  // diagnostics build: per-warp cycle counters into `out` (results wrong)
 #define PKV_ADIAG 0
 #endif
-#ifndef PKV_AMINB2  // the same for G <= 8 (NG = 2)
-#define PKV_AMINB2 4
+#ifndef PKV_AMINB2  // the same for G <= 8 (NG = 2: 3 CTAs per SM measured 1408 -> 1271 us on config E)
+#define PKV_AMINB2 3
 #endif
 #ifndef PKV_AREGC  // pack width constants in registers (1) or from the shared table (0)
 #define PKV_AREGC 0
 #endif
 #ifndef PKV_AMINB  // CTAs per SM the register allocation must allow
-#define PKV_AMINB 4
+#define PKV_AMINB 3
 #endif
 constexpr int kRBA = PKV_RBA, kNSA = PKV_NSA;
 using FeedA = Feed<kRBA, kNSA, PKV_APF, true>;
@@ -685,10 +685,10 @@ __global__ void __launch_bounds__(128 * kMQ) attn_merge_kernel(pkv_layer_t L, in
       l = fmaf(e, ls, l);
     };
     int s = qq;
-    for (; s + 3 * kMQ < ns; s += 4 * kMQ) {  // four slots' loads in flight
-      float Mv[4], av[4], zv[4], lv[4];
+    for (; s + 7 * kMQ < ns; s += 8 * kMQ) {  // eight slots' loads in flight (one round for <= 64 slots)
+      float Mv[8], av[8], zv[8], lv[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 8; ++i) {
         const float* ps = pg + (s + i * kMQ) * st;
         Mv[i] = ps[kD + 2];
         av[i] = ps[c];
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(128 * kMQ) attn_merge_kernel(pkv_layer_t L, in
         lv[i] = ps[kD + 1];
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) fold(Mv[i], av[i], zv[i], lv[i]);
+      for (int i = 0; i < 8; ++i) fold(Mv[i], av[i], zv[i], lv[i]);
     }
     for (; s < ns; s += kMQ) {
       const float* ps = pg + s * st;

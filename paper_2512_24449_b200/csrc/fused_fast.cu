@@ -436,8 +436,8 @@ constexpr int kWV = 4;
 #ifndef PKV_VMINB  // V: CTAs per SM the register allocation must allow
 #define PKV_VMINB 4
 #endif
-#ifndef PKV_VMINB2  // the same for the G <= 8 instantiation (two n-tiles)
-#define PKV_VMINB2 4
+#ifndef PKV_VMINB2  // the same for the G <= 8 instantiation (two n-tiles: 168 registers, no spills; config E V 624 -> 514 us)
+#define PKV_VMINB2 3
 #endif
 #ifndef PKV_RBV  // V ring: 11 KB still fits 4 register-bound CTAs per SM (measured ~2% over 10 KB)
 #define PKV_RBV 11264
