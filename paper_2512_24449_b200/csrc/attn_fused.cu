@@ -51,6 +51,9 @@ constexpr int kResRows = 32;          // residue rows per range item
 #ifndef PKV_AMINB2  // the same for G <= 8 (NG = 2: 3 CTAs per SM measured 1408 -> 1271 us on config E)
 #define PKV_AMINB2 3
 #endif
+#ifndef PKV_AABS  // absolute bit addressing of staged blocks (fast_common.cuh dbase / abase)
+#define PKV_AABS 1
+#endif
 #ifndef PKV_AREGC  // pack width constants in registers (1) or from the shared table (0)
 #define PKV_AREGC 0
 #endif
@@ -93,6 +96,11 @@ __global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
   F.init(wsm + kTileA, lane);
   F.NI = NI;
   __syncthreads();
+  // decode loop (PDL): the prologue above overlaps the previous kernel (the
+  // layer's append-flush); the tables, arena and staging rows it writes are
+  // read only after it completes
+  pdl_wait();
+  pdl_launch();
   const uint32_t tile_s = smem_u32(tile);
   const uint8_t* lutb = (const uint8_t*)lut;
   const uint32_t R0 = 128u * (lane >> 3) + 64u * (lane & 1) + ((lane >> 1) & 3);
@@ -408,11 +416,17 @@ __global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
             // lane walks chunk cidx: its own (K: the transpose tile's order) or
             // chunk 8tq + gi (V: the A fragment's order); minima of that chunk are in ch.mn
             const int cidx = ph ? src : lane;
+#if PKV_AABS
+            uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, cidx) + abase(bp);
+            const auto db = dbase(bp);
+#else
             uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, cidx);
+            const auto db = bp;
+#endif
             const uint2 nb = ph ? ld64(bp + kNib + 8 * src) : ch.nb;
             auto decode = [&](auto wide) {
               uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
-              PackLd A = pack_load<PKV_AREGC>(bp, lutb, bit, wa), B = pack_load<PKV_AREGC>(bp, lutb, bit + wa, wb);
+              PackLd A = pack_load<PKV_AREGC>(db, lutb, bit, wa), B = pack_load<PKV_AREGC>(db, lutb, bit + wa, wb);
 #pragma unroll
               for (int mt = 0; mt < 8; ++mt) {
                 uint32_t P[2][4];
@@ -424,11 +438,11 @@ __global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
                 if (i2 < 14) {
                   nwa = w16_of(nb, i2 + 2);
                   nwb = w16_of(nb, i2 + 3);
-                  nA = pack_load<PKV_AREGC>(bp, lutb, nbit, nwa);
-                  nB = pack_load<PKV_AREGC>(bp, lutb, nbit + nwa, nwb);
+                  nA = pack_load<PKV_AREGC>(db, lutb, nbit, nwa);
+                  nB = pack_load<PKV_AREGC>(db, lutb, nbit + nwa, nwb);
                 }
-                pack_decode<decltype(wide)::value>(bp, A, bitA, wa, min_rep(ch.mn, i2), P[0]);
-                pack_decode<decltype(wide)::value>(bp, B, bitB, wb, min_rep(ch.mn, i2 + 1), P[1]);
+                pack_decode<decltype(wide)::value>(db, A, bitA, wa, min_rep(ch.mn, i2), P[0]);
+                pack_decode<decltype(wide)::value>(db, B, bitB, wb, min_rep(ch.mn, i2 + 1), P[1]);
                 bit = nbit;
                 wa = nwa;
                 wb = nwb;
@@ -664,6 +678,8 @@ __global__ void __launch_bounds__(128 * kMQ) attn_merge_kernel(pkv_layer_t L, in
   __shared__ float rm[kMQ], rz[kMQ], rl[kMQ], ro[kMQ][kD];
   const int c = threadIdx.x & 127, qq = threadIdx.x >> 7;
   const int U = L.batch * L.heads, Hq = L.heads * G;
+  pdl_wait();  // the partials of attn_fused_kernel
+  pdl_launch();
   for (int ug = blockIdx.x; ug < U * G; ug += gridDim.x) {
     const int u = ug / G, g = ug - u * G;
     const int64_t w0 = warp_of(int64_t(u) * NI, total, nwarps), w1 = warp_of(int64_t(u + 1) * NI - 1, total, nwarps);
@@ -806,16 +822,16 @@ int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G
     cudaError_t e = cudaMemsetAsync(cnt, 0, U * sizeof(int), s);
     if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): counters");
   }
-  if (G <= 4)
-    attn_fused_kernel<1><<<p.grid, kWA * 32, a_smem_bytes(), s>>>(*L, q, G, p.NB, p.NI, p.total, p.nchunks, part,
-                                                                  p.maxseg, cnt, out);
-  else
-    attn_fused_kernel<2><<<p.grid, kWA * 32, a_smem_bytes(), s>>>(*L, q, G, p.NB, p.NI, p.total, p.nchunks, part,
-                                                                  p.maxseg, cnt, out);
+  cudaError_t e = G <= 4 ? pkv_launch_pdl(attn_fused_kernel<1>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB,
+                                           p.NI, p.total, p.nchunks, part, p.maxseg, cnt, out)
+                         : pkv_launch_pdl(attn_fused_kernel<2>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB,
+                                           p.NI, p.total, p.nchunks, part, p.maxseg, cnt, out);
+  if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass)");
   if (!cnt && !PKV_ADIAG) {
     const int ug = int(U) * G;
-    attn_merge_kernel<<<ug < 148 * 2 ? ug : 148 * 2, 128 * kMQ, 0, s>>>(*L, G, p.NI, p.total, p.nchunks, part,
-                                                                        p.maxseg, out);
+    e = pkv_launch_pdl(attn_merge_kernel, ug < 148 * 2 ? ug : 148 * 2, 128 * kMQ, 0, s, *L, G, p.NI, p.total,
+                       p.nchunks, (const float*)part, p.maxseg, out);
+    if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): merge");
   }
   return pkv_cuda_status(cudaGetLastError(), "pkv_attention_decode(single pass)");
 }

@@ -1,6 +1,7 @@
 // capi.cu — error reporting and version for the C ABI (include/packkv_b200.h).
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "pkv_common.cuh"
 
@@ -8,6 +9,14 @@ static thread_local char g_last_error[512] = "";
 static thread_local int g_last_path = PKV_PATH_NONE;
 
 void pkv_note_path(int path) { g_last_path = path; }
+
+bool pkv_pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PKV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 void pkv_set_error(const char* fmt, ...) {
   va_list ap;

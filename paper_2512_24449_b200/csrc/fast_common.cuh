@@ -206,6 +206,14 @@ __device__ __forceinline__ PackLd pack_load(P blk, const uint8_t* __restrict__ l
   }
   return r;
 }
+// Pack addressing: a block staged in shared memory is walked with the absolute
+// bit address abase(blk) + bit and a zero base (one shift and mask per pack
+// instead of two plus an add); a block read in place keeps its pointer.
+__device__ __forceinline__ uint32_t dbase(uint32_t) { return 0u; }
+__device__ __forceinline__ const uint8_t* dbase(const uint8_t* p) { return p; }
+__device__ __forceinline__ uint32_t abase(uint32_t a) { return a << 3; }
+__device__ __forceinline__ uint32_t abase(const uint8_t*) { return 0u; }
+
 // r[0..3] = the 16 codes at byte positions 0..15 (see tok()).
 // 4 fields of width w <= 8 at stride w in x -> 4 bytes (fields 0..3), masked,
 // plus mr: the same two-level select tree as spread8 with the 8w-bit halves.
@@ -225,8 +233,7 @@ __device__ __forceinline__ void pack_decode(P blk, const PackLd& L, uint32_t bit
   if (!WIDE || w16 <= 64u) {
     const uint32_t x0 = shf_r_wrap(L.w0, L.w1, bit);  // payload bits 0..31
     const uint32_t x1 = shf_r_wrap(L.w1, L.w2, bit);  // payload bits 32..63
-    const uint32_t md = imad(L.c.x, L.c.x, 0u);       // 2^(32-8w)
-    const uint32_t xh = imad(x1, md, umulhi(x0, md));  // fields 8..15 = payload >> 8w
+    const uint32_t xh = shf_r_clamp(x0, x1, w16 >> 1);  // fields 8..15 = payload >> 8w (8w <= 32)
     spread8(x0, L.c, mr, r[0], r[1]);
     spread8(xh, L.c, mr, r[2], r[3]);
   } else {

@@ -190,9 +190,10 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   #endif
           // the narrow-only loop unless the block holds a pack of width 5..8
           auto decode_packs = [&](auto wide) {
-            uint32_t bit = ch.bit;
+            uint32_t bit = ch.bit + abase(bp);
+            const auto db = dbase(bp);
             uint32_t wa = w16_of(ch.nb, 0), wb = w16_of(ch.nb, 1);
-            PackLd A = pack_load<PKV_KREGC>(bp, lutb, bit, wa), B = pack_load<PKV_KREGC>(bp, lutb, bit + wa, wb);
+            PackLd A = pack_load<PKV_KREGC>(db, lutb, bit, wa), B = pack_load<PKV_KREGC>(db, lutb, bit + wa, wb);
     #pragma unroll
             for (int i2 = 0; i2 < 16; i2 += 2) {
               const uint32_t bitA = bit, bitB = bit + wa;
@@ -202,16 +203,16 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
               if (i2 < 14) {
                 nwa = w16_of(ch.nb, i2 + 2);
                 nwb = w16_of(ch.nb, i2 + 3);
-                nA = pack_load<PKV_KREGC>(bp, lutb, nbit, nwa);
-                nB = pack_load<PKV_KREGC>(bp, lutb, nbit + nwa, nwb);
+                nA = pack_load<PKV_KREGC>(db, lutb, nbit, nwa);
+                nB = pack_load<PKV_KREGC>(db, lutb, nbit + nwa, nwb);
               }
               uint32_t ra[4], rb[4];
     #if PKV_DIAG_NODECODE
               ra[0] = A.w0 ^ bitA; ra[1] = A.w1; ra[2] = A.w2; ra[3] = A.c.x;
               rb[0] = B.w0 ^ bitB; rb[1] = B.w1; rb[2] = B.w2; rb[3] = B.c.x;
     #else
-              pack_decode<decltype(wide)::value>(bp, A, bitA, wa, min_rep(ch.mn, i2), ra);
-              pack_decode<decltype(wide)::value>(bp, B, bitB, wb, min_rep(ch.mn, i2 + 1), rb);
+              pack_decode<decltype(wide)::value>(db, A, bitA, wa, min_rep(ch.mn, i2), ra);
+              pack_decode<decltype(wide)::value>(db, B, bitB, wb, min_rep(ch.mn, i2 + 1), rb);
     #endif
     #if PKV_DIAG_NOSTS
               dsum ^= ra[0] ^ ra[1] ^ ra[2] ^ ra[3] ^ rb[0] ^ rb[1] ^ rb[2] ^ rb[3];
@@ -663,14 +664,15 @@ __global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fu
       __syncwarp();  // frag reads done (the slow path reuses the area)
       if (fast) {
         // lane (gi, tq) = chunk 8tq + gi of the scan (its minima are in ch.mn)
-        uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src);
+        uint32_t bit = __shfl_sync(PKV_FULL, ch.bit, src) + abase(blk);
+        const auto db = dbase(blk);
         const uint2 nb = ld64(blk + kNib + 8 * src);
         const uint32_t (&mn)[8] = ch.mn;
         // the m-tile's two packs decoded together, the next pair's loads in flight
         auto decode_mma = [&](auto wide) {
 #if PKV_VPIPE
           uint32_t wa = w16_of(nb, 0), wb = w16_of(nb, 1);
-          PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
+          PackLd A = pack_load(db, lutb, bit, wa), B = pack_load(db, lutb, bit + wa, wb);
 #endif
   #pragma unroll
           for (int mt = 0; mt < 8; ++mt) {
@@ -679,9 +681,9 @@ __global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fu
             {  // no cross-pair load pipelining: fewer live registers, latency hidden by more warps
               const int i2 = 2 * mt;
               const uint32_t wa = w16_of(nb, i2), wb = w16_of(nb, i2 + 1);
-              const PackLd A = pack_load(blk, lutb, bit, wa), B = pack_load(blk, lutb, bit + wa, wb);
-              pack_decode<decltype(wide)::value>(blk, A, bit, wa, min_rep(mn, i2), P[0]);
-              pack_decode<decltype(wide)::value>(blk, B, bit + wa, wb, min_rep(mn, i2 + 1), P[1]);
+              const PackLd A = pack_load(db, lutb, bit, wa), B = pack_load(db, lutb, bit + wa, wb);
+              pack_decode<decltype(wide)::value>(db, A, bit, wa, min_rep(mn, i2), P[0]);
+              pack_decode<decltype(wide)::value>(db, B, bit + wa, wb, min_rep(mn, i2 + 1), P[1]);
               bit += wa + wb;
             }
 #else
@@ -694,11 +696,11 @@ __global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fu
               if (i2 < 14) {
                 nwa = w16_of(nb, i2 + 2);
                 nwb = w16_of(nb, i2 + 3);
-                nA = pack_load(blk, lutb, nbit, nwa);
-                nB = pack_load(blk, lutb, nbit + nwa, nwb);
+                nA = pack_load(db, lutb, nbit, nwa);
+                nB = pack_load(db, lutb, nbit + nwa, nwb);
               }
-              pack_decode<decltype(wide)::value>(blk, A, bitA, wa, min_rep(mn, i2), P[0]);
-              pack_decode<decltype(wide)::value>(blk, B, bitB, wb, min_rep(mn, i2 + 1), P[1]);
+              pack_decode<decltype(wide)::value>(db, A, bitA, wa, min_rep(mn, i2), P[0]);
+              pack_decode<decltype(wide)::value>(db, B, bitB, wb, min_rep(mn, i2 + 1), P[1]);
               bit = nbit;
               wa = nwa;
               wb = nwb;
@@ -773,7 +775,7 @@ __global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fu
       if (gblk)
         process(gblk, false);
       else
-        process(F.ring + (sblk - smem_u32(F.ring)), true);  // a pointer into the ring: the compiler emits LDS
+        process(sblk, true);  // the shared-window address (LDS, 32-bit addressing)
     }
     F.refill(L, 1, NB, rg, nk, k, F.tail_after(k), lane);
   }

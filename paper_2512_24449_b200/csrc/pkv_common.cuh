@@ -11,6 +11,7 @@
 // and column c; pos(c) = c for the V layout and the stride-4 interleave
 // pos(c) = sum_{r < c%4} ceil((cols-r)/4) + c/4 for the K layout.
 #pragma once
+#include <utility>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -131,6 +132,14 @@ __device__ __forceinline__ bool rs_writer(int lane) {
   return (lane & ((1 << low) - 1)) == 0;
 }
 
+// Programmatic dependent launch (the decode-step kernels, launched with
+// pkv_launch_pdl): the next kernel of the stream may start its prologue while
+// this one runs; pdl_wait() blocks until the previous kernel has completed and
+// its writes are visible, pdl_launch() lets the next kernel start.  Both are
+// no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void set_flag(int32_t* err, int32_t bit) {
   if (err) atomicOr(err, bit);
 }
@@ -150,6 +159,29 @@ __device__ __forceinline__ int res_rows(const pkv_layer_t& L, int b, int64_t str
 }  // namespace pkv
 
 // host-side helpers (defined in capi.cu)
+bool pkv_pdl_enabled();  // PKV_PDL=0 disables programmatic dependent launch
+// <<<grid, block, smem, stream>>> with programmatic stream serialization
+// allowed (the kernel must call pdl_wait() before reading what the previous
+// kernel writes)
+template <typename... KArgs, typename... Args>
+cudaError_t pkv_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                           Args&&... args) {
+  if (!pkv_pdl_enabled()) {
+    kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 void pkv_set_error(const char* fmt, ...);
 int pkv_cuda_status(cudaError_t e, const char* what);
 void pkv_note_path(int path);  // records the kernel family for pkv_last_path()
