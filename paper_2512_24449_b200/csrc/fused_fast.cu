@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, c
   long long dwait = 0;
   const long long tstart = clock64();
 #endif
+  // PDL: only the shared-memory prologue overlaps the previous kernel (which
+  // may be the compressor writing the tables and arena this launch reads)
+  pdl_wait();
+  pdl_launch();
   F.refill(L, 0, NB, rg, nk, -1, 0u, lane);
 
 #pragma unroll 1
@@ -558,13 +562,17 @@ __global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fu
   Cursor cs, cn;
   cs.init(rg.b0, NB, L.heads);
   cn = cs;
-  load_w(0, cn);
   int cur_u = -1, b = 0, h = 0;
 #if PKV_DIAG_WAITCLK
   long long dwait = 0;
   const long long tstart = clock64();
 #endif
+  // PDL: only the shared-memory prologue overlaps the previous kernel (the K
+  // launch writing the scores, or a compressor writing the tables)
+  pdl_wait();
+  pdl_launch();
   F.refill(L, 1, NB, rg, nk, -1, 0u, lane);
+  load_w(0, cn);
 
 #pragma unroll 1
   for (int k = 0; k < nk; ++k) {
@@ -809,6 +817,8 @@ __global__ void __launch_bounds__(512) fused_v_fast_finalize(pkv_layer_t L, cons
   __shared__ float Msh;
   const int U = L.batch * L.heads;
   const int c = threadIdx.x & 127, qq = threadIdx.x >> 7;
+  pdl_wait();  // the V partials
+  pdl_launch();
   for (int ug = blockIdx.x; ug < U * G; ug += gridDim.x) {
     const int u = ug / G, g = ug - u * G;
     if (SM && threadIdx.x < 32) {
@@ -960,11 +970,11 @@ void launch_k(const pkv_layer_t* L, int nblocks, const float* q, int G, float* s
   const int NB = max(1, nblocks);
   const int grid = k_grid<ST>(L, nblocks, G);
   if (G <= 4)
-    fused_k_fast_kernel<1, ST><<<grid, kWK * 32, k_smem_bytes(), s>>>(*L, q, G, scores, sstride, NB, total, kmax, kres,
-                                                                       kslots);
+    pkv_launch_pdl(fused_k_fast_kernel<1, ST>, grid, kWK * 32, k_smem_bytes(), s, *L, q, G, scores, sstride, NB, total,
+                   kmax, kres, kslots);
   else
-    fused_k_fast_kernel<2, ST><<<grid, kWK * 32, k_smem_bytes(), s>>>(*L, q, G, scores, sstride, NB, total, kmax, kres,
-                                                                       kslots);
+    pkv_launch_pdl(fused_k_fast_kernel<2, ST>, grid, kWK * 32, k_smem_bytes(), s, *L, q, G, scores, sstride, NB, total,
+                   kmax, kres, kslots);
 }
 
 template <bool SM>
@@ -978,16 +988,15 @@ void launch_v(const pkv_layer_t* L, int nblocks, const float* w, int G, int64_t 
   float* vscr = part + int64_t(L->batch) * L->heads * maxseg * G * kPart;
   if (total > 0) {
     if (G <= 4)
-      fused_v_fast_kernel<1, SM><<<grid, kWV * 32, v_smem_bytes(), s>>>(*L, w, G, wstride, part, NB, total, maxseg,
-                                                                         vscr, kmax, kres, kslots, knwarps, total);
+      pkv_launch_pdl(fused_v_fast_kernel<1, SM>, grid, kWV * 32, v_smem_bytes(), s, *L, w, G, wstride, part, NB, total,
+                     maxseg, vscr, kmax, kres, kslots, knwarps, total);
     else
-      fused_v_fast_kernel<2, SM><<<grid, kWV * 32, v_smem_bytes(), s>>>(*L, w, G, wstride, part, NB, total, maxseg,
-                                                                         vscr, kmax, kres, kslots, knwarps, total);
+      pkv_launch_pdl(fused_v_fast_kernel<2, SM>, grid, kWV * 32, v_smem_bytes(), s, *L, w, G, wstride, part, NB, total,
+                     maxseg, vscr, kmax, kres, kslots, knwarps, total);
   }
   const int ug = L->batch * L->heads * G;
-  fused_v_fast_finalize<SM><<<ug < 148 * 4 ? ug : 148 * 4, 512, 0, s>>>(*L, part, w, G, wstride, NB, total, nwarps,
-                                                                          maxseg, out, kmax, kres, kslots, knwarps,
-                                                                          total);
+  pkv_launch_pdl(fused_v_fast_finalize<SM>, ug < 148 * 4 ? ug : 148 * 4, 512, 0, s, *L, (const float*)part, w, G,
+                 wstride, NB, total, nwarps, maxseg, out, kmax, kres, kslots, knwarps, total);
 }
 
 }  // namespace
