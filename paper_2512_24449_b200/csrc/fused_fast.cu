@@ -81,6 +81,9 @@ constexpr int kWK = 4;               // warps per CTA
 // 69.8 us for a 10 KB ring at 3 CTAs per SM (config B)
 #define PKV_RBK 5888
 #endif
+#ifndef PKV_KMINB  // K: CTAs per SM the register allocation must allow (1: no bound)
+#define PKV_KMINB 1
+#endif
 #ifndef PKV_NSK
 #define PKV_NSK 3
 #endif
@@ -94,7 +97,7 @@ constexpr size_t kWarpSmemK = (kTile + FeedK::bytes() + 127) / 128 * 128;
 // every (unit, warp slot, head) in kmax[u][slot][g] and of the residue rows in
 // kres[u][g] (-inf when there are none).
 template <int NU, bool ST>  // NU: unsigned query digit tiles, 1 for G <= 4, 2 for G <= 8
-__global__ void __launch_bounds__(kWK * 32) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
+__global__ void __launch_bounds__(kWK * 32, PKV_KMINB) fused_k_fast_kernel(pkv_layer_t L, const float* __restrict__ q, int G,
                                                                  float* __restrict__ scores, int64_t sstride, int NB,
                                                                  int64_t total, float* __restrict__ kmax,
                                                                  float* __restrict__ kres, int kslots) {
