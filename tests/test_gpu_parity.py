@@ -780,7 +780,8 @@ def test_randomized_end_to_end_parity(seed):
     w = rng.random((B, H * G, T)).astype(np.float32)
     s = F.fused_k_scores_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
     o = F.fused_v_output_batched(st, 0, torch.from_numpy(w)).cpu().numpy()
-    a = attention_decode_batched(st, 0, torch.from_numpy(q)).cpu().numpy()
+    a = attention_decode_batched(st, 0, torch.from_numpy(q), single_pass=True).cpu().numpy()
+    a3 = attention_decode_batched(st, 0, torch.from_numpy(q), single_pass=False).cpu().numpy()
     for b in range(B):
         ref = O.OracleStore(1, H, D, rel_k=rel_k, rel_v=rel_v, repack=repack)
         ref.compress_batch(0, kk[b], vv[b])
@@ -791,7 +792,9 @@ def test_randomized_end_to_end_parity(seed):
             _close(o[b, hq], O.naive_v_output(ref, 0, hq // G, w[b, hq]))
             x = rs / np.sqrt(D)
             p = np.exp(x - x.max())
-            _close(a[b, hq], O.naive_v_output(ref, 0, hq // G, p / p.sum()))
+            ra = O.naive_v_output(ref, 0, hq // G, p / p.sum())
+            _close(a[b, hq], ra)   # single pass
+            _close(a3[b, hq], ra)  # three launches
 
 
 @pytest.mark.parametrize("seed", range(24))

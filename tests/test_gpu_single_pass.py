@@ -165,3 +165,41 @@ def test_single_pass_softmax_edges():
     q = (rng.standard_normal(D) * 60).astype(np.float32)
     out = _single(N, A, st, torch.from_numpy(q[None, None])).cpu().numpy()
     _close(out[0, 0], _oracle_attention(ref, 0, q))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_randomized_decode_loop(seed):
+    """GraphedDecodeLoop (append-flush + attention per layer, one graph replay per
+    step; either attention path) against eager append_token + attention on a
+    twin store, over random batch / heads / groups / prefill / headroom and enough
+    steps to cross block completions and a re-capture; streams byte-identical."""
+    N, A, CS = _mods()
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeLoop
+    rng = np.random.default_rng(7000 + seed)
+    B, H, G, Ly = int(rng.integers(1, 4)), int(rng.integers(1, 5)), int(rng.choice([1, 2, 4, 8])), int(rng.integers(1, 3))
+    T0, steps, headroom = int(rng.integers(1, 200)), int(rng.integers(60, 140)), int(rng.integers(1, 3))
+    D = 128
+    k = (rng.standard_normal((Ly, B, T0 + steps, H, D)) * 2).astype(np.float16)
+    v = rng.standard_normal((Ly, B, T0 + steps, H, D)).astype(np.float16)
+    q = rng.standard_normal((steps, Ly, B, H * G, D)).astype(np.float32)
+    a, r = CS(Ly, H, D, batch=B, check=False), CS(Ly, H, D, batch=B, check=False)
+    for l in range(Ly):
+        a.compress_batch(l, k[l, :, :T0], v[l, :, :T0])
+        r.compress_batch(l, k[l, :, :T0], v[l, :, :T0])
+    loop = GraphedDecodeLoop(a, H * G, headroom=headroom)
+    loop.single_pass = bool(seed % 2)
+    kd, vd, qd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    worst = 0.0
+    for t in range(steps):
+        out = loop.step(kd[:, :, T0 + t:T0 + t + 1], vd[:, :, T0 + t:T0 + t + 1], qd[t]).clone()
+        for l in range(Ly):
+            r.append_token(l, kd[l, :, T0 + t], vd[l, :, T0 + t])
+            ref = A(r, l, qd[t, l], single_pass=loop.single_pass)  # the same path (f32 order, digit scaling)
+            worst = max(worst, float((out[l] - ref).abs().max() / ref.abs().max()))
+    assert worst <= 1e-5, worst
+    torch.cuda.synchronize()
+    a.check_errors()
+    for l in range(Ly):
+        assert a[l].nblk_h == r[l].nblk_h and a[l].nres_h == r[l].nres_h
+        for b in range(B):
+            assert a[l].stream_bytes(b) == r[l].stream_bytes(b)
