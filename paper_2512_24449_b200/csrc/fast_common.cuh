@@ -447,6 +447,7 @@ struct Feed {
   int lenl;          // -1: no block (past nblk)
   int NI = 0;        // range items per unit (0: NB)
   int base = 0;      // feed index of the current range's first item (ranges fed one after another)
+  int stride = 1;    // item i of the range is block rg.b0 + i * stride (CTA round-robin: the warp count)
 
   __device__ __forceinline__ void init(uint8_t* smem, int lane) {
     ring = smem;
@@ -470,7 +471,7 @@ struct Feed {
   __device__ __forceinline__ void load_dir(const pkv_layer_t& L, int kind, int NB, const Range& rg, int kk, int lane) {
     k0 = kk;
     const int it = kk + lane - base;
-    const int64_t gb = rg.b0 + (PAIRED ? (it >> 1) : it);
+    const int64_t gb = rg.b0 + int64_t(PAIRED ? (it >> 1) : it) * stride;
     const int kd = PAIRED ? (it & 1) : kind;
     const int ni = NI ? NI : NB;
     offl = 0;

@@ -13,8 +13,16 @@ for _ in range(3):
     F.fused_v_output_batched(st, 0, w)
 torch.cuda.synchronize()
 d = st[0].v_scratch.view(torch.int64)[:3 * 2368].cpu().numpy().reshape(-1, 3)
-d = d[d[:, 2] > 0]
+sm = d[:, 2] >> 32
+d[:, 2] &= 0xffffffff
+keep = d[:, 2] > 0
+d, sm = d[keep], sm[keep]
 wt, t, n = d[:, 0].astype(float), d[:, 1].astype(float), d[:, 2]
+per_sm = np.array([t[sm == s].mean() for s in range(sm.max() + 1) if (sm == s).any()])
+print("per-SM mean loop cycles: min %.0f max %.0f std %.0f; within-SM std (mean over SMs) %.0f" % (
+    per_sm.min(), per_sm.max(), per_sm.std(), np.mean([t[sm == s].std() for s in range(sm.max() + 1) if (sm == s).sum() > 1])))
+order = np.argsort(per_sm)
+print("slowest SMs", order[-8:], "fastest", order[:8])
 print(f"warps {len(d)}  blocks/warp {n.mean():.1f}  loop cycles mean {t.mean():.0f} max {t.max():.0f}")
 print(f"wait share mean {np.mean(wt / t):.3f}  median {np.median(wt / t):.3f}  p90 {np.percentile(wt / t, 90):.3f}")
 print(f"wait cycles per block {np.mean(wt / n):.0f}  loop cycles per block {np.mean(t / n):.0f}")
