@@ -812,7 +812,9 @@ __global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fu
     long long* dbg = reinterpret_cast<long long*>(part) + 3 * wid;
     dbg[0] = dwait;
     dbg[1] = clock64() - tstart;
-    dbg[2] = nk;
+    unsigned smid;  // blocks | SM id << 32 (tools/exp/waitclk_v.py)
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    dbg[2] = nk | (int64_t(smid) << 32);
   }
   return;
 #endif
