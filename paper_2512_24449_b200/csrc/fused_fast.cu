@@ -81,6 +81,9 @@ constexpr int kWK = 4;               // warps per CTA
 // 69.8 us for a 10 KB ring at 3 CTAs per SM (config B)
 #define PKV_RBK 5888
 #endif
+#ifndef PKV_KRR
+#define PKV_KRR 0
+#endif
 #ifndef PKV_KMINB  // K: CTAs per SM the register allocation must allow (1: no bound)
 #define PKV_KMINB 1
 #endif
@@ -120,8 +123,19 @@ __global__ void __launch_bounds__(kWK * 32, PKV_KMINB) fused_k_fast_kernel(pkv_l
   const uint32_t st_even = 16u * ((R0 & ~7u) | ((R0 & 7u) ^ X));
   const uint32_t st_odd = 16u * ((R0 & ~7u) | (((R0 & 7u) | 4u) ^ X));
   const int64_t nwarps = int64_t(gridDim.x) * kWK, wid = int64_t(blockIdx.x) * kWK + warp;
+#if PKV_KRR  // experiment: CTA ranges dealt round-robin to the warps (non-ST only)
+  const Range crg = warp_range(total, blockIdx.x, int64_t(gridDim.x));
+  Range rg;
+  rg.b0 = crg.b0 + warp;
+  rg.b1 = crg.b1;
+  const int nk = rg.b1 > rg.b0 ? int((rg.b1 - rg.b0 + kWK - 1) / kWK) : 0;
+  F.stride = kWK;
+  constexpr int kStepK = kWK;
+#else
   const Range rg = warp_range(total, wid, nwarps);
   const int nk = int(rg.b1 - rg.b0);
+  constexpr int kStepK = 1;
+#endif
 #if PKV_Q2
   QFrag2<NU> Q;
 #else
@@ -156,7 +170,7 @@ __global__ void __launch_bounds__(kWK * 32, PKV_KMINB) fused_k_fast_kernel(pkv_l
   F.refill(L, 0, NB, rg, nk, -1, 0u, lane);
 
 #pragma unroll 1
-  for (int k = 0; k < nk; ++k, cs.step(1, NB, L.heads)) {
+  for (int k = 0; k < nk; ++k, cs.step(kStepK, NB, L.heads)) {
     const int u = cs.u, j = cs.j;
     if (u != cur_u) {
       if (ST && cur_u >= 0) flush_max(cur_u);
