@@ -71,11 +71,37 @@ __device__ __forceinline__ float ldcg_f(const float* p) { return __ldcg(p); }
 // Items per unit: the blocks, then ceil(buffer / 32) residue chunks.
 __host__ __device__ __forceinline__ int res_items(int buffer) { return (buffer + kResRows - 1) / kResRows; }
 
+// The work split over the layer's (unit, item) sequence, from the DEVICE block
+// counts: a decode graph sizes `NB` with headroom for blocks appended later
+// (GraphedDecodeLoop, up to 16 block-sets), and splitting the empty items too
+// put two real items on warps that could have had one.  Items per unit NI =
+// NBd + RI with NBd = the largest nblk[b], clamped to [NB - kNbSlack, NB] (the
+// host sizes the partial slots for that range).  Warp-collective.
+constexpr int kNbSlack = 64;
+#ifndef PKV_ACHUNKS  // work split: chunks per warp of the grid
+#define PKV_ACHUNKS 1
+#endif
+struct ASplit {
+  int NB, NI;
+  int64_t total, nchunks;
+};
+__device__ __forceinline__ ASplit attn_split(const pkv_layer_t& L, int NB, int RI, int64_t nwarps, int lane) {
+  int m = 0;
+  for (int b = lane; b < L.batch; b += 32) m = max(m, L.nblk[b]);
+  m = int(__reduce_max_sync(PKV_FULL, unsigned(m)));
+  ASplit sp;
+  sp.NB = max(max(min(NB, m), NB - kNbSlack), 0);
+  sp.NI = sp.NB + RI;
+  sp.total = int64_t(L.batch) * L.heads * sp.NI;
+  const int64_t want = nwarps * PKV_ACHUNKS;
+  sp.nchunks = want < sp.total ? want : (sp.total > 0 ? sp.total : 1);
+  return sp;
+}
+
 template <int NG>  // NG = 1: G <= 4 (one digit tile / n-tile), 2: G <= 8
 __global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
-    attn_fused_kernel(pkv_layer_t L, const float* __restrict__ q, int G, int NB, int NI, int64_t total,
-                      int64_t nchunks, float* __restrict__ part, int maxseg,
-                      int* __restrict__ cnt, float* __restrict__ out) {
+    attn_fused_kernel(pkv_layer_t L, const float* __restrict__ q, int G, int NBh, int RI,
+                      float* __restrict__ part, int maxseg, int* __restrict__ cnt, float* __restrict__ out) {
   constexpr int GP = 4 * NG;     // padded heads
   constexpr int LPH = 32 / GP;   // writer lanes per head
   constexpr int TPL = 64 / LPH;  // rows per writer lane (8 or 16)
@@ -94,13 +120,16 @@ __global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
   float* qsm = (float*)(wsm + 3072);           // [G][128] residue chunks: the q copy (K step)
   FeedA F;
   F.init(wsm + kTileA, lane);
-  F.NI = NI;
   __syncthreads();
   // decode loop (PDL): the prologue above overlaps the previous kernel (the
   // layer's append-flush); the tables, arena and staging rows it writes are
   // read only after it completes
   pdl_wait();
   pdl_launch();
+  const ASplit sp = attn_split(L, NBh, RI, int64_t(gridDim.x) * kWA, lane);
+  const int NB = sp.NB, NI = sp.NI;
+  const int64_t total = sp.total, nchunks = sp.nchunks;
+  F.NI = NI;
   const uint32_t tile_s = smem_u32(tile);
   const uint8_t* lutb = (const uint8_t*)lut;
   const uint32_t R0 = 128u * (lane >> 3) + 64u * (lane & 1) + ((lane >> 1) & 3);
@@ -672,14 +701,18 @@ __global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
 // of channel c with an online maximum, then the kMQ groups are combined in a
 // fixed order.  out = sum_s e^(M_s - M*) (acc_s + z_s) / sum_s e^(M_s - M*) l_s.
 constexpr int kMQ = 8;
-__global__ void __launch_bounds__(128 * kMQ) attn_merge_kernel(pkv_layer_t L, int G, int NI, int64_t total,
-                                                             int64_t nwarps, const float* __restrict__ part,
+__global__ void __launch_bounds__(128 * kMQ) attn_merge_kernel(pkv_layer_t L, int G, int NBh, int RI,
+                                                             int64_t fwarps, const float* __restrict__ part,
                                                              int maxseg, float* __restrict__ out) {
   __shared__ float rm[kMQ], rz[kMQ], rl[kMQ], ro[kMQ][kD];
   const int c = threadIdx.x & 127, qq = threadIdx.x >> 7;
   const int U = L.batch * L.heads, Hq = L.heads * G;
   pdl_wait();  // the partials of attn_fused_kernel
   pdl_launch();
+  // the attention kernel's split (fwarps: its warps), from the same device counts
+  const ASplit sp = attn_split(L, NBh, RI, fwarps, threadIdx.x & 31);
+  const int NI = sp.NI;
+  const int64_t total = sp.total, nwarps = sp.nchunks;
   for (int ug = blockIdx.x; ug < U * G; ug += gridDim.x) {
     const int u = ug / G, g = ug - u * G;
     const int64_t w0 = warp_of(int64_t(u) * NI, total, nwarps), w1 = warp_of(int64_t(u + 1) * NI - 1, total, nwarps);
@@ -772,9 +805,6 @@ int attn_grid_cap(K kernel) {
   return cap;
 }
 
-#ifndef PKV_ACHUNKS  // work split: chunks per warp of the grid
-#define PKV_ACHUNKS 1
-#endif
 struct AttnPlan {
   int NB, NI, grid, maxseg, G;
   int64_t total, nchunks;
@@ -792,9 +822,17 @@ AttnPlan attn_plan(const pkv_layer_t* L, int nblocks, int G) {
   p.grid = int(want < 1 ? 1 : (want < cap ? want : cap));
   const int64_t nwarps = int64_t(p.grid) * kWA;
   p.nchunks = nwarps * PKV_ACHUNKS < p.total ? nwarps * PKV_ACHUNKS : (p.total > 0 ? p.total : 1);
-  // slots per unit: the most chunks whose ranges can meet one unit
-  const int64_t len_min = p.total / p.nchunks;
-  p.maxseg = len_min == 0 ? int(p.NI < p.nchunks ? p.NI : p.nchunks) + 1 : int((p.NI + len_min - 1) / len_min + 1);
+  // slots per unit: the most chunks whose ranges can meet one unit, over every
+  // device block count the kernels may split by (attn_split)
+  const int RI = res_items(L->buffer);
+  p.maxseg = 1;
+  for (int nb = max(0, p.NB - kNbSlack); nb <= p.NB; ++nb) {
+    const int64_t ni = nb + RI, tot = U * ni;
+    const int64_t nch = nwarps * PKV_ACHUNKS < tot ? nwarps * PKV_ACHUNKS : (tot > 0 ? tot : 1);
+    const int64_t len_min = tot / nch;
+    const int ms = len_min == 0 ? int(ni < nch ? ni : nch) + 1 : int((ni + len_min - 1) / len_min + 1);
+    p.maxseg = max(p.maxseg, ms);
+  }
   return p;
 }
 
@@ -822,15 +860,16 @@ int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G
     cudaError_t e = cudaMemsetAsync(cnt, 0, U * sizeof(int), s);
     if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): counters");
   }
+  const int RI = res_items(L->buffer);
   cudaError_t e = G <= 4 ? pkv_launch_pdl(attn_fused_kernel<1>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB,
-                                           p.NI, p.total, p.nchunks, part, p.maxseg, cnt, out)
+                                           RI, part, p.maxseg, cnt, out)
                          : pkv_launch_pdl(attn_fused_kernel<2>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB,
-                                           p.NI, p.total, p.nchunks, part, p.maxseg, cnt, out);
+                                           RI, part, p.maxseg, cnt, out);
   if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass)");
   if (!cnt && !PKV_ADIAG) {
     const int ug = int(U) * G;
-    e = pkv_launch_pdl(attn_merge_kernel, ug < 148 * 2 ? ug : 148 * 2, 128 * kMQ, 0, s, *L, G, p.NI, p.total,
-                       p.nchunks, (const float*)part, p.maxseg, out);
+    e = pkv_launch_pdl(attn_merge_kernel, ug < 148 * 2 ? ug : 148 * 2, 128 * kMQ, 0, s, *L, G, p.NB, RI,
+                       int64_t(p.grid) * kWA, (const float*)part, p.maxseg, out);
     if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): merge");
   }
   return pkv_cuda_status(cudaGetLastError(), "pkv_attention_decode(single pass)");
