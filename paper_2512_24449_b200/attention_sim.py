@@ -39,7 +39,7 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
     softmax and V block by block, then a deterministic merge of the per-warp
     partials; no score row reaches HBM); False the three-launch path, which
     also fills `scores`.  Default (None): the single pass when `scores` is not
-    requested and the layer is latency-bound (few blocks per resident warp,
+    requested and the layer is latency-bound (at most 4 items per resident warp,
     single_pass_preferred), where it measured faster (config C: 622 vs 482
     tokens/s); the three-launch path at long contexts, where its two
     kernels issue faster (config B 131 vs 140 us)."""
@@ -88,7 +88,7 @@ def attention_decode_batched(store: CompressedStore, layer: int, q, score_stride
 # resident warps of the fused kernels on a B200 (148 SMs x 16) and the
 # blocks-per-warp crossover below which the single pass is the faster path
 _RESIDENT_WARPS = 148 * 16
-SINGLE_PASS_MAX_ITEMS_PER_WARP = 8
+SINGLE_PASS_MAX_ITEMS_PER_WARP = 4  # config B shape: parity at 3.6 items per warp (8K tokens), three launches 10% faster at 7.1 (16K)
 
 
 def single_pass_preferred(store: CompressedStore, nblocks: int) -> bool:

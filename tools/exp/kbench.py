@@ -12,7 +12,10 @@ ap.add_argument("which", nargs="*", default=["k", "v"])
 ap.add_argument("--cfg", default="B")
 ap.add_argument("--reps", type=int, default=30)
 a = ap.parse_args()
-cfg = bench.CONFIGS[a.cfg]
+if a.cfg.startswith("BL"):  # config B shape at another context length, e.g. BL4352
+    cfg = (8, 8, 32, 128, int(a.cfg[2:]), f"config B shape at {a.cfg[2:]} tokens")
+else:
+    cfg = bench.CONFIGS[a.cfg]
 B, Hkv, Hq, D, L = cfg[:5]
 st = bench.build_store(cfg, 0)
 ls = st[0]
