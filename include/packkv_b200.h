@@ -189,6 +189,13 @@ int pkv_flush_staged(const pkv_layer_t* L, float rel_k, float rel_v, void* scrat
  * once before first use (as for pkv_flush_staged).                         */
 int pkv_append_flush(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new, float rel_k, float rel_v,
                      void* scratch, int64_t scratch_bytes, void* stream);
+/* pkv_append_flush for a ragged decode batch: only sequences with
+ * active[b] != 0 (device uint8 [B]; NULL = all) append this step, so their
+ * lengths diverge on the device (nblk[b], nres[b]); the fused kernels and
+ * attention already follow each sequence's own counts.                     */
+int pkv_append_flush_masked(const pkv_layer_t* L, const uint16_t* k_new, const uint16_t* v_new,
+                            const uint8_t* active, float rel_k, float rel_v, void* scratch, int64_t scratch_bytes,
+                            void* stream);
 /* Appends `ntok` tokens to every sequence (lockstep batch).  k_new/v_new:
  * [B][ntok][H][D] fp16.  `staged` = tokens already staged per sequence
  * (host mirror of nres, < block); `nblocks_before` = blocks per sequence

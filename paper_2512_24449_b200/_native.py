@@ -76,6 +76,8 @@ _SIGS = {
     "pkv_attention_decode": (c_int32, [POINTER(Layer), c_int32, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p,
                                        c_int64, c_void_p]),
     "pkv_append_flush": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_float, c_float, c_void_p, c_int64, c_void_p]),
+    "pkv_append_flush_masked": (c_int32, [POINTER(Layer), c_void_p, c_void_p, c_void_p, c_float, c_float, c_void_p,
+                                          c_int64, c_void_p]),
 }
 
 _lib = None

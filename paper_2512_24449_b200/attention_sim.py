@@ -310,6 +310,14 @@ class GraphedDecodeLoop:
         self.v = torch.zeros_like(self.k)
         self.q = torch.zeros((n, B, q_heads, D), dtype=torch.float32, device=dev)
         self.out = torch.empty((n, B, q_heads, D), dtype=torch.float32, device=dev)
+        # ragged decode: active[b] = 1 appends sequence b's token this step
+        self.active = torch.ones(B, dtype=torch.uint8, device=dev)
+        self._active_all = True
+        import numpy as np
+        self._seq_nblk = [np.full(B, store[l].nblk_h, np.int64) for l in self.layers] if not any(
+            store[l].ragged for l in self.layers) else [store[l].nblk.cpu().numpy().astype(np.int64) for l in self.layers]
+        self._seq_nres = [np.full(B, store[l].nres_h, np.int64) for l in self.layers] if not any(
+            store[l].ragged for l in self.layers) else [store[l].nres.cpu().numpy().astype(np.int64) for l in self.layers]
         self._flush_scr = [None] * n
         self._scores = [None] * n
         self._cap = [0] * n
@@ -363,9 +371,10 @@ class GraphedDecodeLoop:
             ls = o[l]
             L = ctypes_ref(ls.struct())
             if with_append and self.fused_append:
-                N.check(lib.pkv_append_flush(L, N.ptr(self.k[i]), N.ptr(self.v[i]), float(o.rel_scale_k),
-                                             float(o.rel_scale_v), N.ptr(self._flush_scr[i]),
-                                             int(self._flush_scr[i].numel()), N.stream()), "append_flush")
+                N.check(lib.pkv_append_flush_masked(L, N.ptr(self.k[i]), N.ptr(self.v[i]), N.ptr(self.active),
+                                                    float(o.rel_scale_k), float(o.rel_scale_v),
+                                                    N.ptr(self._flush_scr[i]), int(self._flush_scr[i].numel()),
+                                                    N.stream()), "append_flush")
             else:
                 if with_append:
                     N.check(lib.pkv_stage_token(L, N.ptr(self.k[i]), N.ptr(self.v[i]), N.stream()), "stage_token")
@@ -398,25 +407,44 @@ class GraphedDecodeLoop:
         self._key = self._state()
         self.captures += 1
 
-    def step(self, k=None, v=None, q=None) -> torch.Tensor:
+    def step(self, k=None, v=None, q=None, active=None) -> torch.Tensor:
+        """active (optional, [B] bool / 0-1): the sequences that append a token
+        this step (the others only attend); their lengths then diverge on the
+        device (a ragged batch, pkv_append_flush_masked)."""
+        import numpy as np
         o = self.store
         for dst, src in ((self.k, k), (self.v, v), (self.q, q)):
             if src is not None and src.data_ptr() != dst.data_ptr():
                 dst.copy_(src.reshape(dst.shape), non_blocking=True)
+        if active is None:
+            act = np.ones(o.batch, bool)
+            if not bool(self._active_all):
+                self.active.fill_(1)
+                self._active_all = True
+        else:
+            act = np.asarray(active.cpu() if isinstance(active, torch.Tensor) else active, dtype=bool).reshape(-1)
+            if act.shape != (o.batch,):
+                raise E.ShapeMismatchError(f"active must have {o.batch} entries")
+            if not self.fused_append and not act.all():
+                raise ValueError("an active mask needs fused_append (pkv_append_flush_masked)")
+            self.active.copy_(torch.from_numpy(act.astype(np.uint8)), non_blocking=True)
+            self._active_all = bool(act.all())
         # the graph covers blocks j < cap: re-capture once a flush could create block cap
         need = any(o[l].nblk_h >= self._cap[i] for i, l in enumerate(self.layers))
         if self._graph is None or need or self._state() != self._key:
             self._capture()
         self._graph.replay()
-        for l in self.layers:  # host mirrors follow the device (lockstep batch)
+        for i, l in enumerate(self.layers):  # host mirrors follow the device, sequence by sequence
             ls = o[l]
-            ls.nres_h += 1
-            if ls.nres_h == o.block:
-                ls.nres_h = 0
-                ls.nblk_h += 1
-                ls.tail_ub += 2 * o.batch * o.heads * ls.blk_max
+            nres, nblk = self._seq_nres[i], self._seq_nblk[i]
+            nres[act] += 1
+            done = nres >= o.block
+            nblk[done] += 1
+            nres[done] -= o.block
+            ls.tail_ub += int(done.sum()) * 2 * o.heads * ls.blk_max
+            ls.nblk_h, ls.nres_h = int(nblk.max()), int(nres.max())
+            ls.ragged = ls.ragged or not (np.all(nblk == nblk[0]) and np.all(nres == nres[0]))
         return self.out
-
 
 def attention_decode(store: CompressedStore, layer: int, head: int, q) -> torch.Tensor:
     """SPEC.md:520-528 (batch 1, one head)."""

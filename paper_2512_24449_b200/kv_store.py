@@ -93,6 +93,10 @@ class LayerStore:
         self.a_scratch = torch.empty(0, dtype=torch.uint8, device=dev)
         # host mirrors
         self.nblk_h = 0
+        # True once the sequences' lengths diverge (GraphedDecodeLoop with an
+        # active mask): nblk_h / nres_h then hold the largest counts (sizing
+        # only); the device nblk[b] / nres[b] are each sequence's own
+        self.ragged = False
         self.nres_h = 0
         self.tail_ub = 0
         self._struct = None
@@ -161,6 +165,8 @@ class LayerStore:
         store's own strategy is used otherwise."""
         o = self.owner
         T = int(k_new.shape[1])
+        if self.ragged:
+            raise ValueError("ragged batch (sequences of different lengths): append through GraphedDecodeLoop")
         lib = N.lib()
         strm = N.stream()
         if check and T:
@@ -221,6 +227,8 @@ class LayerStore:
         device residue count (pkv_stage_token), so the launch is identical
         every step and can live inside a CUDA graph (GraphedDecodeStep)."""
         o = self.owner
+        if self.ragged:
+            raise ValueError("ragged batch (sequences of different lengths): append through GraphedDecodeLoop")
         if self.nres_h + 1 >= o.block:
             raise ValueError("this token completes a block: use compress()")
         N.check(N.lib().pkv_stage_token(ctypes_ref(self.struct()), N.ptr(k_new), N.ptr(v_new), N.stream()),
@@ -275,6 +283,8 @@ class LayerStore:
                 for kind in (KIND_K, KIND_V):
                     for h in range(o.heads):
                         u = b * o.heads + h
+                        if off[kind, u, j] < 0:  # a ragged batch: sequence b has no block j yet
+                            continue
                         ents.append(BlockDirectoryEntry(kind, self.layer, h, j * o.block, (j + 1) * o.block,
                                                         int(off[kind, u, j]), int(ln[kind, u, j]),
                                                         pm[b, j].astype(np.int64), b))
@@ -447,8 +457,11 @@ _PKKS_REC = np.dtype([("off", "<u8"), ("len", "<u4")])
 
 
 def save_store(store: CompressedStore, path) -> None:
-    """Serialize every layer (synchronises the device)."""
+    """Serialize every layer (synchronises the device).  The PKKS format holds
+    one (blocks, residue) count per layer: a ragged batch cannot be saved."""
     o = store
+    if any(ls.ragged for ls in o.layer_stores):
+        raise E.StoreFormatError("ragged batch: PKKS stores one block / residue count per layer")
     with open(path, "wb") as f:
         f.write(_PKKS_HDR.pack(b"PKKS", 1, o.layers, o.batch, o.heads, o.head_dim, o.block, o.pack_size, o.buffer,
                                N.REPACK[o.repack], o.rel_scale_k, o.rel_scale_v))

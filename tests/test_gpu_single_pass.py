@@ -203,3 +203,59 @@ def test_randomized_decode_loop(seed):
         assert a[l].nblk_h == r[l].nblk_h and a[l].nres_h == r[l].nres_h
         for b in range(B):
             assert a[l].stream_bytes(b) == r[l].stream_bytes(b)
+
+
+@pytest.mark.parametrize("single", [True, False])
+def test_ragged_decode_loop(single):
+    """A ragged decode batch: each step a random subset of the sequences appends
+    its next token (GraphedDecodeLoop.step(active=...), pkv_append_flush_masked)
+    and every sequence attends over its own history.  Each sequence must match
+    a batch-1 store fed only its own tokens (eager append_token + attention),
+    and its packed stream must be byte-identical to that store's."""
+    N, A, CS = _mods()
+    from paper_2512_24449_b200 import errors as E
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeLoop
+    rng = np.random.default_rng(31 + int(single))
+    B, H, G, Ly, D = 3, 2, 4, 2, 128
+    T0, steps = 50, 180
+    k = rng.standard_normal((Ly, B, T0 + steps, H, D)).astype(np.float16)
+    v = rng.standard_normal((Ly, B, T0 + steps, H, D)).astype(np.float16)
+    q = rng.standard_normal((steps, Ly, B, H * G, D)).astype(np.float32)
+    a = CS(Ly, H, D, batch=B, check=False)
+    refs = [CS(Ly, H, D, batch=1, check=False) for _ in range(B)]
+    for l in range(Ly):
+        a.compress_batch(l, k[l, :, :T0], v[l, :, :T0])
+        for b in range(B):
+            refs[b].compress_batch(l, k[l, b:b + 1, :T0], v[l, b:b + 1, :T0])
+    loop = GraphedDecodeLoop(a, H * G, headroom=2)
+    loop.single_pass = single
+    kd, vd, qd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    pos = np.full(B, T0)
+    worst = 0.0
+    for t in range(steps):
+        act = rng.random(B) < 0.7
+        act[t % B] = True if t < 3 else act[t % B]
+        kin = torch.stack([kd[:, b, pos[b]] for b in range(B)], 1)[:, :, None]   # [Ly, B, 1, H, D]
+        vin = torch.stack([vd[:, b, pos[b]] for b in range(B)], 1)[:, :, None]
+        out = loop.step(kin, vin, qd[t], active=act).clone()
+        for b in range(B):
+            for l in range(Ly):
+                if act[b]:
+                    refs[b].append_token(l, kd[l, b, pos[b]][None], vd[l, b, pos[b]][None])
+                ref = A(refs[b], l, qd[t, l, b][None], single_pass=single)[0]
+                worst = max(worst, float((out[l, b] - ref).abs().max() / ref.abs().max()))
+        pos += act
+    assert worst <= 1e-5, worst
+    torch.cuda.synchronize()
+    a.check_errors()
+    assert any(a[l].ragged for l in range(Ly)) and len(set(pos.tolist())) > 1
+    for l in range(Ly):
+        assert a[l].nblk.tolist() == [refs[b][l].nblk_h for b in range(B)]
+        assert a[l].nres.tolist() == [refs[b][l].nres_h for b in range(B)]
+        for b in range(B):
+            assert a[l].stream_bytes(b) == refs[b][l].stream_bytes(0), f"layer {l} seq {b}"
+    with pytest.raises(ValueError):  # eager appends need a lockstep batch
+        a.append_token(0, kd[0, :, 0], vd[0, :, 0])
+    with pytest.raises(E.StoreFormatError):
+        from paper_2512_24449_b200.kv_store import save_store
+        save_store(a, "/tmp/ragged.pkks")
