@@ -313,11 +313,9 @@ class GraphedDecodeLoop:
         # ragged decode: active[b] = 1 appends sequence b's token this step
         self.active = torch.ones(B, dtype=torch.uint8, device=dev)
         self._active_all = True
-        import numpy as np
-        self._seq_nblk = [np.full(B, store[l].nblk_h, np.int64) for l in self.layers] if not any(
-            store[l].ragged for l in self.layers) else [store[l].nblk.cpu().numpy().astype(np.int64) for l in self.layers]
-        self._seq_nres = [np.full(B, store[l].nres_h, np.int64) for l in self.layers] if not any(
-            store[l].ragged for l in self.layers) else [store[l].nres.cpu().numpy().astype(np.int64) for l in self.layers]
+        counts = [store[l].seq_counts() for l in self.layers]
+        self._seq_nblk = [c[0] for c in counts]
+        self._seq_nres = [c[1] for c in counts]
         self._flush_scr = [None] * n
         self._scores = [None] * n
         self._cap = [0] * n

@@ -205,6 +205,46 @@ class LayerStore:
         if check:
             N.raise_flags(int(self.err.item()), "compress")
 
+    def append_masked(self, k_new: torch.Tensor, v_new: torch.Tensor, counts, check: bool = False):
+        """Ragged append: sequence b appends its first counts[b] tokens of
+        k_new / v_new ([B, T, H, D] fp16), one masked step per token position
+        (pkv_append_flush_masked: the token staged at the device residue count,
+        a completed block compressed in the same launch)."""
+        o = self.owner
+        counts = np.asarray(counts, dtype=np.int64)
+        lib = N.lib()
+        if check:
+            for x in (k_new, v_new):
+                N.check(lib.pkv_check_finite(N.ptr(x), x.numel(), N.ptr(self.err), N.stream()), "append")
+            N.raise_flags(int(self.err.item()), "append")
+        nb0, nr0 = self.seq_counts()
+        n = nr0 + counts
+        self._ensure(int((n // o.block).max()) + 1)
+        fb = int(lib.pkv_flush_scratch_bytes(ctypes_ref(self.struct())))
+        if getattr(self, "flush_scr", None) is None or self.flush_scr.numel() < fb:
+            self.flush_scr = torch.zeros(fb, dtype=torch.uint8, device=o.device)  # zero before first use
+        active = torch.empty(o.batch, dtype=torch.uint8, device=o.device)
+        for t in range(int(counts.max(initial=0))):
+            active.copy_(torch.from_numpy((counts > t).astype(np.uint8)))
+            kt, vt = k_new[:, t].contiguous(), v_new[:, t].contiguous()  # alive until the launch is enqueued
+            N.check(lib.pkv_append_flush_masked(ctypes_ref(self.struct()), N.ptr(kt), N.ptr(vt), N.ptr(active),
+                                                float(o.rel_scale_k), float(o.rel_scale_v), N.ptr(self.flush_scr),
+                                                int(self.flush_scr.numel()), N.stream()), "append_masked")
+        nblk, nres = nb0 + n // o.block, n % o.block
+        self.tail_ub += int((n // o.block).sum()) * 2 * o.heads * self.blk_max
+        self.nblk_h, self.nres_h = int(nblk.max()), int(nres.max())
+        self.ragged = self.ragged or not (np.all(nblk == nblk[0]) and np.all(nres == nres[0]))
+        if check:
+            N.raise_flags(int(self.err.item()), "append_masked")
+
+    def seq_counts(self):
+        """Per-sequence (blocks, staged tokens) as int64 arrays [B]: the host
+        mirrors for a lockstep batch, the device counts for a ragged one."""
+        o = self.owner
+        if not self.ragged:
+            return np.full(o.batch, self.nblk_h, np.int64), np.full(o.batch, self.nres_h, np.int64)
+        return self.nblk.cpu().numpy().astype(np.int64), self.nres.cpu().numpy().astype(np.int64)
+
     def pending_codes(self, k_new: torch.Tensor, v_new: torch.Tensor):
         """Quantized codes of the block-sets that appending k_new/v_new
         ([B, T, H, D] fp16, device) would complete, without appending:
@@ -372,20 +412,40 @@ class CompressedStore:
         v = self._norm(v_vec, False)
         ls.compress(k, v, self.check)
 
-    def compress_batch(self, layer: int, k_tokens, v_tokens):
-        """identical final state to appending token by token."""
+    def compress_batch(self, layer: int, k_tokens, v_tokens, lengths=None):
+        """identical final state to appending token by token.
+
+        lengths (optional, [B]): a ragged prefill -- sequence b takes its first
+        lengths[b] tokens of k_tokens / v_tokens ([B, T, H, D], T >= max).  The
+        common prefix is compressed in lockstep, the rest appended one step at a
+        time for the sequences that still have tokens (pkv_append_flush_masked,
+        default format, repack none); the store is then ragged (see
+        GraphedDecodeLoop)."""
         ls = self[layer]
         k = self._norm(k_tokens, True)
         v = self._norm(v_tokens, True)
         if k.shape != v.shape:
             raise E.ShapeMismatchError("K and V batches differ in shape")
-        ls.compress(k, v, self.check)
+        if lengths is None:
+            ls.compress(k, v, self.check)
+            return
+        lens = np.asarray(lengths, dtype=np.int64).reshape(-1)
+        if lens.shape != (self.batch,) or (lens < 0).any() or lens.max(initial=0) > k.shape[1]:
+            raise E.ShapeMismatchError(f"lengths must be {self.batch} counts <= {k.shape[1]}")
+        common = int(lens.min())
+        ls.compress(k[:, :common].contiguous(), v[:, :common].contiguous(), self.check)
+        if common == int(lens.max()):
+            return
+        if self.repack != "none" or self.pack_size != 16 or self.head_dim != 128 or self.block != 64:
+            raise ValueError("ragged prefill: default format with repack none only")
+        ls.append_masked(k[:, common:], v[:, common:], lens - common, self.check)
 
     def iterate_blocks(self, layer: int, kind: int, seq: int = 0):
         """directory entries of (layer, kind) then the residue handle."""
         ls = self[layer]
         ents = [e for e in ls.directory() if e.kind == kind and e.seq == seq]
-        return ents + [ResidueHandle(layer, ls.nblk_h * self.block, ls.nres_h, seq)]
+        nb, nr = ls.seq_counts()
+        return ents + [ResidueHandle(layer, int(nb[seq]) * self.block, int(nr[seq]), seq)]
 
     def shrink_to_fit(self, headroom_bytes: int = 0):
         """Release the arena capacity reserved beyond the compressed bytes (every layer)."""

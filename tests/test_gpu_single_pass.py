@@ -259,3 +259,46 @@ def test_ragged_decode_loop(single):
     with pytest.raises(E.StoreFormatError):
         from paper_2512_24449_b200.kv_store import save_store
         save_store(a, "/tmp/ragged.pkks")
+
+
+def test_ragged_prefill_then_decode():
+    """compress_batch(lengths=...) builds a ragged store (common prefix in
+    lockstep, the rest as masked append steps); every sequence's stream, block
+    table and attention equal a batch-1 store of its own tokens, then the
+    decode loop keeps going from the ragged state."""
+    N, A, CS = _mods()
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeLoop
+    rng = np.random.default_rng(12)
+    B, H, G, D = 3, 2, 4, 128
+    lens = np.array([100, 37, 200])
+    T = 260
+    k = rng.standard_normal((B, T, H, D)).astype(np.float16)
+    v = rng.standard_normal((B, T, H, D)).astype(np.float16)
+    st = CS(1, H, D, batch=B, check=False)
+    st.compress_batch(0, k, v, lengths=lens)
+    refs = [CS(1, H, D, batch=1, check=False) for _ in range(B)]
+    for b in range(B):
+        refs[b].compress_batch(0, k[b:b + 1, :lens[b]], v[b:b + 1, :lens[b]])
+    assert st[0].ragged
+    assert st[0].nblk.tolist() == [r[0].nblk_h for r in refs] and st[0].nres.tolist() == [r[0].nres_h for r in refs]
+    q = rng.standard_normal((B, H * G, D)).astype(np.float32)
+    out = A(st, 0, torch.from_numpy(q), single_pass=True).cpu().numpy()
+    for b in range(B):
+        assert st[0].stream_bytes(b) == refs[b][0].stream_bytes(0)
+        ref = A(refs[b], 0, torch.from_numpy(q[b:b + 1]), single_pass=True).cpu().numpy()[0]
+        _close(out[b], ref)
+        assert len(st.iterate_blocks(0, 0, b)) == H * (lens[b] // 64) + 1  # every head's K blocks + the residue
+    loop = GraphedDecodeLoop(st, H * G, headroom=2)
+    pos = lens.copy()
+    for t in range(40):
+        kin = torch.from_numpy(np.stack([k[b, pos[b]] for b in range(B)])[None, :, None]).cuda()
+        vin = torch.from_numpy(np.stack([v[b, pos[b]] for b in range(B)])[None, :, None]).cuda()
+        qt = torch.from_numpy(rng.standard_normal((1, B, H * G, D)).astype(np.float32)).cuda()
+        o = loop.step(kin, vin, qt).clone()
+        for b in range(B):
+            refs[b].append_token(0, torch.from_numpy(k[b, pos[b]][None]).cuda(), torch.from_numpy(v[b, pos[b]][None]).cuda())
+            r = A(refs[b], 0, qt[0, b:b + 1], single_pass=loop.single_pass)[0]
+            assert float((o[0, b] - r).abs().max() / r.abs().max()) <= 1e-5
+        pos += 1
+    for b in range(B):
+        assert st[0].stream_bytes(b) == refs[b][0].stream_bytes(0)
