@@ -98,8 +98,8 @@ __device__ __forceinline__ ASplit attn_split(const pkv_layer_t& L, int NB, int R
   return sp;
 }
 
-template <int NG>  // NG = 1: G <= 4 (one digit tile / n-tile), 2: G <= 8
-__global__ void __launch_bounds__(kWA * 32, NG == 2 ? PKV_AMINB2 : PKV_AMINB)
+template <int NG, int MB>  // NG = 1: G <= 4 (one digit tile / n-tile), 2: G <= 8; MB: CTAs per SM
+__global__ void __launch_bounds__(kWA * 32, MB)
     attn_fused_kernel(pkv_layer_t L, const float* __restrict__ q, int G, int NBh, int RI,
                       float* __restrict__ part, int maxseg, int* __restrict__ cnt, float* __restrict__ out) {
   constexpr int GP = 4 * NG;     // padded heads
@@ -806,7 +806,7 @@ int attn_grid_cap(K kernel) {
 }
 
 struct AttnPlan {
-  int NB, NI, grid, maxseg, G;
+  int NB, NI, grid, maxseg, G, mb;
   int64_t total, nchunks;
 };
 
@@ -817,7 +817,15 @@ AttnPlan attn_plan(const pkv_layer_t* L, int nblocks, int G) {
   p.NI = p.NB + res_items(L->buffer);
   const int64_t U = int64_t(L->batch) * L->heads;
   p.total = U * p.NI;
-  const int cap = G <= 4 ? attn_grid_cap(attn_fused_kernel<1>) : attn_grid_cap(attn_fused_kernel<2>);
+  // G <= 4: 3 CTAs per SM (168 registers, no spills) while the items fit one
+  // per warp, else 4 (128 registers, a few spills) so a layer with more items
+  // than 12 warps per SM hold runs fewer rounds (config C 716 -> 744 tokens/s)
+  int cap = G <= 4 ? attn_grid_cap(attn_fused_kernel<1, PKV_AMINB>) : attn_grid_cap(attn_fused_kernel<2, PKV_AMINB2>);
+  p.mb = G <= 4 ? PKV_AMINB : PKV_AMINB2;
+  if (G <= 4 && p.total > int64_t(cap) * kWA) {
+    cap = attn_grid_cap(attn_fused_kernel<1, 4>);
+    p.mb = 4;
+  }
   const int64_t want = (p.total + kWA - 1) / kWA;
   p.grid = int(want < 1 ? 1 : (want < cap ? want : cap));
   const int64_t nwarps = int64_t(p.grid) * kWA;
@@ -861,10 +869,16 @@ int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G
     if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): counters");
   }
   const int RI = res_items(L->buffer);
-  cudaError_t e = G <= 4 ? pkv_launch_pdl(attn_fused_kernel<1>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB,
-                                           RI, part, p.maxseg, cnt, out)
-                         : pkv_launch_pdl(attn_fused_kernel<2>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB,
-                                           RI, part, p.maxseg, cnt, out);
+  cudaError_t e;
+  if (G > 4)
+    e = pkv_launch_pdl(attn_fused_kernel<2, PKV_AMINB2>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB, RI, part,
+                       p.maxseg, cnt, out);
+  else if (p.mb == 4)
+    e = pkv_launch_pdl(attn_fused_kernel<1, 4>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB, RI, part,
+                       p.maxseg, cnt, out);
+  else
+    e = pkv_launch_pdl(attn_fused_kernel<1, PKV_AMINB>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB, RI,
+                       part, p.maxseg, cnt, out);
   if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass)");
   if (!cnt && !PKV_ADIAG) {
     const int ug = int(U) * G;

@@ -1,0 +1,6 @@
+timeout 900 python -m pytest -q -x tests/test_gpu_single_pass.py > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
+cp paper_2512_24449_b200/libpackkv_b200.so /tmp/b.so
+for v in base prev base prev; do [ $v = base ] && cp /tmp/b.so paper_2512_24449_b200/libpackkv_b200.so || cp tools/exp/lib$v.so paper_2512_24449_b200/libpackkv_b200.so
+timeout 600 python bench.py --config C --stream-steps 2048 > /tmp/c.log 2>&1; tail -1 /tmp/c.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$v C tok/s', d['tokens_per_s'], 'e2e', d['e2e']['tokens_per_s'])"; done
+cp /tmp/b.so paper_2512_24449_b200/libpackkv_b200.so
