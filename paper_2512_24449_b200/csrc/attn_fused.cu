@@ -6,9 +6,10 @@
 // "single decompress+compute launch").
 //
 //  * Work split: the layer's (unit, item) sequence, unit = (sequence, kv-head),
-//    items = the unit's NB blocks followed by kResItems chunks of 32 residue
+//    items = the unit's blocks followed by buffer / 32 chunks of 32 residue
 //    rows, is cut into one contiguous equal-length range per warp of the grid
-//    (fast_common.cuh warp_range).
+//    (fast_common.cuh warp_range); the block count comes from the device
+//    counts (attn_split), so a decode graph's headroom adds no empty items.
 //  * Each warp streams the K and V block of every block item through its own
 //    shared-memory ring (PAIRED feed: K then V of the same block), decodes K
 //    into the transpose tile, takes the scores on the int8 tensor cores
@@ -21,10 +22,13 @@
 //  * Residue chunks: the uncompressed fp16 staging rows in f32 SIMT, folded
 //    into the same running state.
 //  * Merge: each (unit, warp) segment writes (acc, z, l, M) to a partial slot;
-//    the warp that completes a unit's last segment (per-unit arrival counter)
-//    merges the unit's slots in slot order, out = sum e^(M_s - M*) (acc_s +
-//    z_s) / sum e^(M_s - M*) l_s, and resets the counter.  The result does not
-//    depend on arrival order (deterministic).
+//    attn_merge_kernel folds a unit's slots in slot order, out = sum
+//    e^(M_s - M*) (acc_s + z_s) / sum e^(M_s - M*) l_s, deterministic
+//    (SPEC.md:487,490).  (PKV_ATTN_INLINE_MERGE=1: the warp completing a
+//    unit's last segment merges it instead, per-unit arrival counters -- a
+//    serial tail at the end of the kernel, measured slower.)
+//  * One decode loop serves the K and the V phase of an item (the code of two
+//    unrolled loops overflowed the instruction cache).
 #include "fast_common.cuh"
 
 #include <cstdlib>
