@@ -27,8 +27,7 @@
 //    (SPEC.md:487,490).  (PKV_ATTN_INLINE_MERGE=1: the warp completing a
 //    unit's last segment merges it instead, per-unit arrival counters -- a
 //    serial tail at the end of the kernel, measured slower.)
-//  * One decode loop serves the K and the V phase of an item (the code of two
-//    unrolled loops overflowed the instruction cache).
+//  * One copy of the unrolled unpack serves the K and the V phase of an item.
 #include "fast_common.cuh"
 
 #include <cstdlib>
@@ -369,9 +368,9 @@ __global__ void __launch_bounds__(kWA * 32, MB)
     if (j < NB) {
       // ============================ block item: K phase, softmax step, V phase.
       // ONE decode loop serves both phases (ph 0: K codes into the transpose
-      // tile; ph 1: V codes straight into the IMMA A operand): two unrolled
-      // decode loops overflow the 32 KB L1.5 instruction cache (ncu: ~1.2
-      // no-instruction stalls per issue against ~0.17 for the K or V kernel).
+      // tile; ph 1: V codes straight into the IMMA A operand), one copy of the
+      // unrolled unpack in the hot loop.  (ncu shows ~1 no-instruction stall
+      // per issue against ~0.17 for the K or V kernel either way.)
 #pragma unroll 1
       for (int ph = 0; ph < 2; ++ph) {
         const uint8_t* gb;
