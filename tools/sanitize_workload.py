@@ -46,7 +46,13 @@ st4.compress_batch(0, k[:, :60], v[:, :60])
 loop = GraphedDecodeLoop(st4, H * G, headroom=2)
 for t in range(60, 72):
     loop.step(k[None, :, t:t + 1], v[None, :, t:t + 1], q[None])
+# ragged: prefill by lengths (masked append-flush), then a masked decode loop
+st5 = CompressedStore(1, H, D, batch=B, check=False)
+st5.compress_batch(0, k[:, :140], v[:, :140], lengths=[140, 70])
+loop5 = GraphedDecodeLoop(st5, H * G, headroom=2)
+for t in range(8):
+    loop5.step(k[None, :, t:t + 1], v[None, :, t:t + 1], q[None], active=[t % 2 == 0, True])
 torch.cuda.synchronize()
-for s in (st, st2, st3, st4):
+for s in (st, st2, st3, st4, st5):
     s.check_errors()
 print("sanitize workload ok")
