@@ -13,14 +13,18 @@ for _ in range(3):
     F.fused_v_output_batched(st, 0, w)
 torch.cuda.synchronize()
 d = st[0].v_scratch.view(torch.int64)[:3 * 2368].cpu().numpy().reshape(-1, 3)
+wid_all = np.arange(len(d))
 sm = d[:, 2] >> 32
 d[:, 2] &= 0xffffffff
 keep = d[:, 2] > 0
-d, sm = d[keep], sm[keep]
+d, sm, wids = d[keep], sm[keep], wid_all[keep]
 wt, t, n = d[:, 0].astype(float), d[:, 1].astype(float), d[:, 2]
 per_sm = np.array([t[sm == s].mean() for s in range(sm.max() + 1) if (sm == s).any()])
 print("per-SM mean loop cycles: min %.0f max %.0f std %.0f; within-SM std (mean over SMs) %.0f" % (
     per_sm.min(), per_sm.max(), per_sm.std(), np.mean([t[sm == s].std() for s in range(sm.max() + 1) if (sm == s).sum() > 1])))
+print("mean loop cycles by warp-in-CTA:", [round(float(t[wids % 4 == w].mean())) for w in range(4)])
+cta = wids // 4
+print("by CTA wave (cta // 148):", [round(float(t[(cta // 148) == c].mean())) for c in range(int(cta.max() // 148) + 1)])
 order = np.argsort(per_sm)
 print("slowest SMs", order[-8:], "fastest", order[:8])
 print(f"warps {len(d)}  blocks/warp {n.mean():.1f}  loop cycles mean {t.mean():.0f} max {t.max():.0f}")
