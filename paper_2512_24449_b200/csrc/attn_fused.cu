@@ -24,13 +24,12 @@
 //  * Merge: each (unit, warp) segment writes (acc, z, l, M) to a partial slot;
 //    attn_merge_kernel folds a unit's slots in slot order, out = sum
 //    e^(M_s - M*) (acc_s + z_s) / sum e^(M_s - M*) l_s, deterministic
-//    (SPEC.md:487,490).  (PKV_ATTN_INLINE_MERGE=1: the warp completing a
-//    unit's last segment merges it instead, per-unit arrival counters -- a
-//    serial tail at the end of the kernel, measured slower.)
+//    (SPEC.md:487,490).  (Having the warp that completes a unit's last
+//    segment merge it, with per-unit arrival counters, left a serial tail at
+//    the end of the kernel and measured slower.)
 //  * One copy of the unrolled unpack serves the K and the V phase of an item.
 #include "fast_common.cuh"
 
-#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -104,7 +103,7 @@ __device__ __forceinline__ ASplit attn_split(const pkv_layer_t& L, int NB, int R
 template <int NG, int MB>  // NG = 1: G <= 4 (one digit tile / n-tile), 2: G <= 8; MB: CTAs per SM
 __global__ void __launch_bounds__(kWA * 32, MB)
     attn_fused_kernel(pkv_layer_t L, const float* __restrict__ q, int G, int NBh, int RI,
-                      float* __restrict__ part, int maxseg, int* __restrict__ cnt, float* __restrict__ out) {
+                      float* __restrict__ part, int maxseg, float* __restrict__ out) {
   constexpr int GP = 4 * NG;     // padded heads
   constexpr int LPH = 32 / GP;   // writer lanes per head
   constexpr int TPL = 64 / LPH;  // rows per writer lane (8 or 16)
@@ -192,75 +191,7 @@ __global__ void __launch_bounds__(kWA * 32, MB)
     }
     Mw = -INFINITY;
     lacc = zacc = 0.f;
-    if (cnt == nullptr) return;  // attn_merge_kernel merges
-    __threadfence();
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) last = atomicAdd(&cnt[u], 1) == int(w1 - w0);
-    last = __shfl_sync(PKV_FULL, last, 0);
-    if (!last) return;
-    __threadfence();
-    const int ns = int(w1 - w0 + 1);
-    const float* pu = part + int64_t(u) * maxseg * G * kPartA;
-    const int64_t st = int64_t(G) * kPartA;
-    const int b = u / L.heads, h = u - b * L.heads;
-    // every head at once (independent loads in flight): slot statistics with
-    // lane s holding slots s, s + 32, ..., then the channel sums in slot order
-    float m[GP], zs[GP], ls[GP];
-#pragma unroll
-    for (int g = 0; g < GP; ++g) m[g] = -INFINITY;
-    for (int s = lane; s < ns; s += 32)
-#pragma unroll
-      for (int g = 0; g < GP; ++g)
-        if (g < G) m[g] = fmaxf(m[g], ldcg_f(pu + s * st + g * kPartA + kD + 2));
-#pragma unroll
-    for (int g = 0; g < GP; ++g) {
-      m[g] = warp_max(m[g]);
-      zs[g] = ls[g] = 0.f;
-    }
-    float4 o[GP];
-#pragma unroll
-    for (int g = 0; g < GP; ++g) o[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < ns; s0 += 32) {
-      const int sl = s0 + lane;
-      float el[GP];
-#pragma unroll
-      for (int g = 0; g < GP; ++g) {
-        el[g] = 0.f;
-        if (g < G && sl < ns) {
-          const float* ps = pu + sl * st + g * kPartA;
-          const float Ms = ldcg_f(ps + kD + 2);
-          el[g] = Ms == -INFINITY ? 0.f : exp2f(Ms - m[g]);
-          zs[g] = fmaf(el[g], ldcg_f(ps + kD), zs[g]);
-          ls[g] = fmaf(el[g], ldcg_f(ps + kD + 1), ls[g]);
-        }
-      }
-      const int n = min(32, ns - s0);
-#pragma unroll 4
-      for (int i = 0; i < n; ++i) {
-        const float* ps = pu + (s0 + i) * st + 4 * lane;
-#pragma unroll
-        for (int g = 0; g < GP; ++g) {
-          const float e = __shfl_sync(PKV_FULL, el[g], i);
-          if (g < G) {
-            const float4 a = __ldcg((const float4*)(ps + g * kPartA));
-            o[g].x = fmaf(e, a.x, o[g].x);
-            o[g].y = fmaf(e, a.y, o[g].y);
-            o[g].z = fmaf(e, a.z, o[g].z);
-            o[g].w = fmaf(e, a.w, o[g].w);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < GP; ++g) {
-      if (g >= G) continue;
-      const float z = warp_sum(zs[g]), l = warp_sum(ls[g]);
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      *(float4*)(out + (int64_t(b) * Hq + int64_t(h) * G + g) * kD + 4 * lane) =
-          make_float4((o[g].x + z) * inv, (o[g].y + z) * inv, (o[g].z + z) * inv, (o[g].w + z) * inv);
-    }
-    if (lane == 0) cnt[u] = 0;  // ready for the next launch
+    // attn_merge_kernel merges the unit's slots
   };
 
   // ---- softmax step over sbuf (raw scores of this item's rows, -inf for rows
@@ -849,41 +780,31 @@ AttnPlan attn_plan(const pkv_layer_t* L, int nblocks, int G) {
 
 }  // namespace
 
-// Scratch: 16 reserved bytes, the inline-merge arrival counters [U], then
-// the partials [U][maxseg][G][kPartA] f32.
+// Scratch: 16 reserved bytes, then the partials [U][maxseg][G][kPartA] f32.
 int64_t pkv_fast_attention1_scratch(const pkv_layer_t* L, int nblocks, int G) {
   const AttnPlan p = attn_plan(L, nblocks, G);
   const int64_t U = int64_t(L->batch) * L->heads;
-  return 16 + (U + 3) / 4 * 16 + U * p.maxseg * G * kPartA * 4;
+  return 16 + U * p.maxseg * G * kPartA * 4;
 }
 
 int pkv_fast_attention1(const pkv_layer_t* L, int nblocks, const float* q, int G, float* out, void* scratch,
                         cudaStream_t s) {
   const AttnPlan p = attn_plan(L, nblocks, G);
   const int64_t U = int64_t(L->batch) * L->heads;
-  static const bool inline_merge = [] {
-    const char* e = getenv("PKV_ATTN_INLINE_MERGE");
-    return e && e[0] == '1';
-  }();
-  int* cnt = inline_merge ? (int*)((uint8_t*)scratch + 16) : nullptr;
-  float* part = (float*)((uint8_t*)scratch + 16 + (U + 3) / 4 * 16);
-  if (cnt) {
-    cudaError_t e = cudaMemsetAsync(cnt, 0, U * sizeof(int), s);
-    if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass): counters");
-  }
+  float* part = (float*)((uint8_t*)scratch + 16);
   const int RI = res_items(L->buffer);
   cudaError_t e;
   if (G > 4)
     e = pkv_launch_pdl(attn_fused_kernel<2, PKV_AMINB2>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB, RI, part,
-                       p.maxseg, cnt, out);
+                       p.maxseg, out);
   else if (p.mb == 4)
     e = pkv_launch_pdl(attn_fused_kernel<1, 4>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB, RI, part,
-                       p.maxseg, cnt, out);
+                       p.maxseg, out);
   else
     e = pkv_launch_pdl(attn_fused_kernel<1, PKV_AMINB>, p.grid, kWA * 32, a_smem_bytes(), s, *L, q, G, p.NB, RI,
-                       part, p.maxseg, cnt, out);
+                       part, p.maxseg, out);
   if (e != cudaSuccess) return pkv_cuda_status(e, "pkv_attention_decode(single pass)");
-  if (!cnt && !PKV_ADIAG) {
+  if (!PKV_ADIAG) {
     const int ug = int(U) * G;
     e = pkv_launch_pdl(attn_merge_kernel, ug < 148 * 2 ? ug : 148 * 2, 128 * kMQ, 0, s, *L, G, p.NB, RI,
                        int64_t(p.grid) * kWA, (const float*)part, p.maxseg, out);
