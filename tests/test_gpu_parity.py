@@ -188,6 +188,25 @@ def test_store_default_format_fast_path(repack):
         assert got == exp
 
 
+@pytest.mark.parametrize("rel", [(1.0, 0.5), (0.34, 0.2), (1 / 15.5, 1 / 16.5), (0.1, 0.2), (0.01, 0.003), (2e-4, 1e-3)])
+def test_store_fast_buffer_bound(rel):
+    """The compressor's per-warp assembly buffer is sized from rel (codes <= round(1/rel),
+    store.cu fastc::buf_bytes); uniform data puts the full code range in nearly every pack,
+    so blocks reach the bound's width, at the power-of-two edges (1/15.5, 1/16.5) too.
+    Bytes equal the oracle's and no flag is raised."""
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(23)
+    B, H, D, T = 2, 2, 128, 64 * 3 + 5
+    kk = rng.uniform(-4, 4, (B, T, H, D)).astype(np.float16)
+    vv = rng.uniform(-1, 3, (B, T, H, D)).astype(np.float16)
+    st = CS(1, H, D, batch=B, rel_scale_k=rel[0], rel_scale_v=rel[1])
+    st.compress_batch(0, kk, vv)
+    for b in range(B):
+        ref = O.OracleStore(1, H, D, rel_k=rel[0], rel_v=rel[1])
+        ref.compress_batch(0, kk[b], vv[b])
+        assert st[0].stream_bytes(b) == ref.layer_stream(0)
+
+
 def test_store_default_format_errors():
     pk, _, _, _, CS = _pk()
     bad = np.zeros((70, 2, 128), np.float16)
