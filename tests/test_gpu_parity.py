@@ -1006,3 +1006,32 @@ def test_randomized_graphed_decode_loop(seed):
     assert a[0].nblk_h == b[0].nblk_h and a[0].nres_h == b[0].nres_h
     for s in range(B):
         assert a[0].stream_bytes(s) == b[0].stream_bytes(s)
+
+
+@pytest.mark.parametrize("repack", ["none", "v_median"])
+def test_iterate_blocks_matches_oracle(repack):
+    """iterate_blocks on the device store: per (layer, kind) the
+    directory entries in order -- head, token range, length, permutation and the
+    block bytes -- then the residue handle, equal to the oracle's after a prefill
+    and token appends that cross block boundaries (two layers)."""
+    _, _, _, _, CS = _pk()
+    rng = np.random.default_rng(31)
+    H, D, T0, A = 3, 128, 64 * 2 + 40, 90
+    st = CS(2, H, D, repack=repack)
+    ref = O.OracleStore(2, H, D, repack=repack)
+    for layer in range(2):
+        kk, vv = _kv(rng, T0 + A, H, D)
+        st.compress_batch(layer, kk[:T0], vv[:T0])
+        ref.compress_batch(layer, kk[:T0], vv[:T0])
+        for t in range(T0, T0 + A):
+            st.append_token(layer, kk[t], vv[t])
+            ref.append_token(layer, kk[t], vv[t])
+    for layer in range(2):
+        for kind in (0, 1):
+            got = st.iterate_blocks(layer, kind)
+            ents, nres = ref.iterate_blocks(layer, kind)
+            blocks, res = got[:-1], got[-1]
+            assert [(e.head, e.token_start, e.token_end, e.byte_len, e.permutation.tolist()) for e in blocks] == \
+                   [(e.head, e.token_start, e.token_end, e.byte_len, e.permutation.tolist()) for e in ents]
+            assert [st[layer].block_bytes(e) for e in blocks] == [ref.block_bytes(e) for e in ents]
+            assert (res.layer, res.tokens, res.token_start) == (layer, nres, (T0 + A) // 64 * 64)
