@@ -85,7 +85,11 @@ constexpr int kWK = 4;               // warps per CTA
 #define PKV_KRR 0
 #endif
 #ifndef PKV_KMINB  // K: CTAs per SM the register allocation must allow (1: no bound)
-#define PKV_KMINB 1
+// 4: <= 128 registers, so the score-statistics (ST, attention) and G <= 8 instantiations
+// (132 / 141-147 registers unbounded, 3 CTAs per SM) also run 4 CTAs = 16 warps per SM, as
+// the shared memory allows: config B three-launch attention 132.0 -> 128.4 us, config E
+// fused K 486 -> 466 us, attention 1026 -> 1009 us (same box, kbench)
+#define PKV_KMINB 4
 #endif
 #ifndef PKV_NSK
 #define PKV_NSK 3
