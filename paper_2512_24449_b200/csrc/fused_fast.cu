@@ -77,7 +77,9 @@ constexpr int kWK = 4;               // warps per CTA
 #endif
 #ifndef PKV_RBK  // ring bytes / slots per K warp (-D overrides for tools/exp variants)
 // 5.9 KB: 8 KB tile + ring fit 4 CTAs of 4 warps per SM (16 warps) and still
-// hold the largest fast-path block (1544 + 512 * 8 B); measured 67.3 us vs
+// hold the largest narrow-width block (w <= 4: 1544 + 512 * 8 B); a block with
+// wider packs (w 5..7, up to ~8.7 KB) that does not fit is decoded in place
+// from global memory (same fast path, global loads); measured 67.3 us vs
 // 69.8 us for a 10 KB ring at 3 CTAs per SM (config B)
 #define PKV_RBK 5888
 #endif
