@@ -741,8 +741,9 @@ def main():
 
     def e2e_step():
         for l in range(layers):
-            o = decs[l].step(q_host[l])  # pinned host q: copied straight into the graph's input buffer
-            out_host[l].copy_(o.reshape(-1), non_blocking=True)
+            # pinned host q in, pinned host out: with one rank both move inside the decode
+            # graph (zero-copy over PCIe, GraphedAttention); with more, out is copied after the gather
+            decs[l].step(q_host[l], out=out_host[l])
 
     for _ in range(args.warmup):
         e2e_step()
@@ -817,10 +818,11 @@ def main():
                        "pass = attn_fused_kernel + attn_merge_kernel, three launch = fused K + fused V + finalize"},
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": layers * Bl * Hql * D * 4,
                     "d2h_bytes_per_step": layers * world * Bl * Hql * D * 4,
-                    "path": "sharding.ShardedDecoder.step (public API) per layer on the pinned host q shard: H2D "
-                            "straight into the graph's input buffer, one CUDA-graph replay of the decode attention "
-                            f"(attention_sim.GraphedAttention, {e2e_attn} path per single_pass_preferred), all-gather "
-                            "of per-head outputs, D2H out",
+                    "path": "sharding.ShardedDecoder.step(q_host, out=host) (public API) per layer on the pinned "
+                            "host q shard: one CUDA-graph replay of the decode attention "
+                            f"(attention_sim.GraphedAttention, {e2e_attn} path per single_pass_preferred) that reads q "
+                            "from host memory (zero-copy, prescaled) and, with one rank, writes the output to host "
+                            "memory; with more ranks all-gather of per-head outputs, then D2H out",
                     "ms_per_step": round(e2e_ms, 5)},
             "memory": mem,
             # scaling with and without the all-gather -- the same

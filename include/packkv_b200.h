@@ -112,6 +112,13 @@ int pkv_quantize(const uint16_t* x, int32_t n, int32_t rows, int32_t cols, float
 /* HalfTensor ingestion check: ORs PKV_FLAG_NONFINITE into *err
  * if any of the n fp16 values is NaN or infinite.                          */
 int pkv_check_finite(const uint16_t* x, int64_t n, int32_t* err, void* stream);
+/* dst = scale * src (n f32).  Either pointer may be pinned host memory (UVA:
+ * the kernel reads / writes it over PCIe directly).  Plumbing of the decode
+ * step's zero-copy I/O (attention_sim.GraphedAttention with host buffers): the
+ * query arrives from host memory with the 1/sqrt(d) prescale applied and the
+ * output leaves to host memory inside one CUDA graph.  No reference
+ * counterpart (SPEC.md:520-528 takes q and returns the output; this moves them). */
+int pkv_copy_scaled(const float* src, float* dst, int64_t n, float scale, void* stream);
 /* dequantize: out = q*scale + zp in f32 (mul then add). */
 int pkv_dequantize(const uint16_t* q, const float* params, int32_t n, int32_t rows,
                    int32_t cols, float* out, void* stream);
@@ -239,7 +246,8 @@ int64_t pkv_attention_scratch_bytes(const pkv_layer_t* L, int32_t nblocks, int32
  *     maxima), fused V on exp(s - M) with the row maximum M, normalising
  *     finalize.
  * q, out and scratch 16-byte aligned; calls sharing a scratch buffer must be
- * stream-ordered.  Default format only (pack 16,
+ * stream-ordered.  out may be pinned host memory (UVA): the last kernel
+ * (finalize / merge) stores each output row to it directly.  Default format only (pack 16,
  * head_dim 128, block 64, G <= 8); else PKV_E_ARG.  Blocks past a
  * sequence's device count nblk[b] (nblocks headroom) are skipped.      */
 int pkv_attention_decode(const pkv_layer_t* L, int32_t nblocks, const float* q, int32_t q_heads, float* scores,

@@ -49,6 +49,7 @@ _SIGS = {
     "pkv_last_path": (c_int32, []),
     "pkv_quantize": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_float, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pkv_check_finite": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "pkv_copy_scaled": (c_int32, [c_void_p, c_void_p, c_int64, c_float, c_void_p]),
     "pkv_dequantize": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "pkv_encode_sizes": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "pkv_encode": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,

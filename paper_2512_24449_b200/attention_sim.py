@@ -136,12 +136,12 @@ class _Captured:
 
     single_pass = None  # None: single_pass_preferred; True / False force a path
 
-    def _attend(self, q: torch.Tensor) -> torch.Tensor:
+    def _attend(self, q: torch.Tensor, prescaled: bool = False, out: torch.Tensor = None) -> torch.Tensor:
         sp = self.single_pass
         if sp is None:
             sp = single_pass_preferred(self.store, self.store[self.layer].nblk_h)
-        return attention_decode_batched(self.store, self.layer, q, scores=self._scores, out=self._out,
-                                        single_pass=sp)
+        return attention_decode_batched(self.store, self.layer, q, scores=self._scores,
+                                        out=self._out if out is None else out, single_pass=sp, prescaled=prescaled)
 
     def _graphable(self, q: torch.Tensor) -> bool:
         """Only the default format's folded-softmax launches (pkv_attention_decode)
@@ -186,13 +186,21 @@ class GraphedAttention(_Captured):
     block count or the device buffers change (every 64 appended tokens, or
     when the store grows)."""
 
-    def __call__(self, q: torch.Tensor) -> torch.Tensor:
-        if (isinstance(q, torch.Tensor) and not q.is_cuda and self._key is not None and q.dtype == torch.float32
-                and tuple(q.shape) == tuple(self._q.shape) and self._state(self._q) == self._key):
-            # a host query (pinned for async) goes straight into the graph's input buffer
-            self._q.copy_(q, non_blocking=True)
-            self._graph.replay()
-            return self._out
+    supports_host_out = True
+
+    def __call__(self, q: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+        """q [B, Hq, D] on the device, or pinned host f32: then the graph reads it from host
+        memory itself (zero-copy over PCIe, with the 1/sqrt(d) prescale, pkv_copy_scaled)
+        instead of a copy-engine transfer before the replay.  out (optional, pinned host f32
+        [B, Hq, D], with a host q) receives the output inside the same graph: the attention's
+        last kernel stores it to host memory directly.  The host
+        buffers' addresses are part of the capture: reuse the same ones every step (static
+        I/O buffers), new ones re-capture."""
+        if isinstance(q, torch.Tensor) and not q.is_cuda and q.dtype == torch.float32 and q.is_pinned() \
+                and q.is_contiguous() and q.dim() == 3:
+            return self._host_call(q, out)
+        if out is not None:
+            raise E.ShapeMismatchError("out= (host output) needs a pinned host f32 q")
         q = _as_f32(q, self.store.device)
         key = self._state(q)
         if key != self._key and not self._graphable(q):
@@ -206,6 +214,36 @@ class GraphedAttention(_Captured):
         self._q.copy_(q, non_blocking=True)
         self._graph.replay()
         return self._out
+
+    def _host_call(self, qh: torch.Tensor, oh: torch.Tensor = None) -> torch.Tensor:
+        if oh is not None and not (not oh.is_cuda and oh.is_pinned() and oh.dtype == torch.float32
+                                   and oh.is_contiguous() and tuple(oh.shape) == tuple(qh.shape)):
+            raise E.ShapeMismatchError(f"out must be a pinned host f32 tensor of shape {tuple(qh.shape)}")
+        hkey = ("host", qh.data_ptr(), oh.data_ptr() if oh is not None else 0)
+        if self._key is None or self._key[-1] != hkey or self._key[:-1] != self._state(self._q):
+            qd = qh.to(self.store.device)
+            if not self._graphable(qd):  # generic format: eager, copies through the copy engine
+                o = attention_decode_batched(self.store, self.layer, qd)
+                if oh is not None:
+                    oh.copy_(o)
+                    return oh
+                return o
+            self._q = torch.empty_like(qd)
+            self._buffers(qd)
+            lib, n = N.lib(), qh.numel()
+            inv = 1.0 / math.sqrt(self.store.head_dim)
+
+            def record():
+                N.check(lib.pkv_copy_scaled(qh.data_ptr(), self._q.data_ptr(), n, inv, N.stream()))
+                # the last kernel (finalize / merge) stores the output straight to the pinned
+                # host buffer (UVA): no device-side output round trip, no copy launch
+                self._attend(self._q, prescaled=True, out=oh)
+
+            record()  # warm-up outside capture
+            self._capture(record)
+            self._key = self._state(self._q) + (hkey,)
+        self._graph.replay()
+        return oh if oh is not None else self._out
 
 
 class GraphedDecodeStep(_Captured):

@@ -112,6 +112,42 @@ extern "C" int pkv_check_finite(const uint16_t* x, int64_t n, int32_t* err, void
   return launch_status("pkv_check_finite");
 }
 
+// dst = scale * src over n f32; either side may be pinned host memory, which
+// the SMs read / write over PCIe directly (UVA), so a decode step's query can
+// arrive from host memory already prescaled and its output leave to host
+// memory inside one CUDA graph, without copy-engine transfers.  float4 when
+// both pointers are 16-byte aligned and n % 4 == 0.
+__global__ void copy_scaled_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n, float scale,
+                                   bool vec) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (vec) {
+    for (; i < n / 4; i += stride) {
+      float4 v = reinterpret_cast<const float4*>(src)[i];
+      v.x *= scale;
+      v.y *= scale;
+      v.z *= scale;
+      v.w *= scale;
+      reinterpret_cast<float4*>(dst)[i] = v;
+    }
+  } else {
+    for (; i < n; i += stride) dst[i] = src[i] * scale;
+  }
+}
+
+extern "C" int pkv_copy_scaled(const float* src, float* dst, int64_t n, float scale, void* stream) {
+  if (n < 0 || (n > 0 && (!src || !dst))) { pkv_set_error("pkv_copy_scaled: bad arguments"); return PKV_E_ARG; }
+  if (n == 0) return PKV_OK;
+  const bool vec = n % 4 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int64_t items = vec ? n / 4 : n;
+  // one element (or float4) per thread up to 148 x 8 CTAs: many small reads in
+  // flight is what a PCIe-mapped source needs
+  const int64_t grid = (items + kThreads - 1) / kThreads;
+  copy_scaled_kernel<<<unsigned(grid < 148 * 8 ? grid : 148 * 8), kThreads, 0, (cudaStream_t)stream>>>(src, dst, n,
+                                                                                                   scale, vec);
+  return launch_status("pkv_copy_scaled");
+}
+
 extern "C" int pkv_dequantize(const uint16_t* q, const float* params, int32_t n, int32_t rows, int32_t cols,
                               float* out, void* stream) {
   const int64_t total = int64_t(n) * rows * cols;

@@ -100,9 +100,19 @@ class ShardedDecoder:
         """Global q [B, Hq, D] -> this rank's [B_loc, Hq_loc, D]."""
         return local_slice(self.p, q, head_axis=1, group=self.G).contiguous()
 
-    def step(self, q_local: torch.Tensor) -> torch.Tensor:
+    def step(self, q_local: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+        """out (optional, host): receives the global output.  With one rank, a pinned host
+        q_local and a local attention that writes host memory itself (GraphedAttention),
+        q and out move inside the decode graph (zero-copy); otherwise out is filled by an
+        asynchronous copy of the gathered result."""
+        if self.p.world == 1 and out is not None and getattr(self.local_attention, "supports_host_out", False) \
+                and not q_local.is_cuda and q_local.is_pinned() and out.is_pinned():
+            return self.local_attention(q_local, out=out.view(q_local.shape))
         out_local = self.local_attention(q_local).contiguous()
         if self.p.world == 1:
+            if out is not None:
+                out.view(out_local.shape).copy_(out_local, non_blocking=True)
+                return out
             return out_local
         shape = (self.p.world,) + tuple(out_local.shape)
         if self._gather is None or self._gather.shape != shape or self._gather.device != out_local.device:
@@ -111,7 +121,11 @@ class ShardedDecoder:
             dist.all_gather_into_tensor(self._gather.view(-1, *out_local.shape[1:]), out_local, group=self.group)
         else:
             dist.all_gather(list(self._gather.unbind(0)), out_local, group=self.group)
-        return assemble(self.p, self._gather)
+        res = assemble(self.p, self._gather)
+        if out is not None:
+            out.view(res.shape).copy_(res, non_blocking=True)
+            return out
+        return res
 
 
 def _all_gather(t: torch.Tensor, world: int, group=None) -> torch.Tensor:

@@ -1035,3 +1035,42 @@ def test_iterate_blocks_matches_oracle(repack):
                    [(e.head, e.token_start, e.token_end, e.byte_len, e.permutation.tolist()) for e in ents]
             assert [st[layer].block_bytes(e) for e in blocks] == [ref.block_bytes(e) for e in ents]
             assert (res.layer, res.tokens, res.token_start) == (layer, nres, (T0 + A) // 64 * 64)
+
+
+def test_graphed_attention_zero_copy_host_io():
+    """GraphedAttention with pinned host q / out: the graph reads q from host memory
+    (pkv_copy_scaled, prescale folded in) and writes the output to host memory; equal to
+    the device-q replay (<= 1e-6 relative), replays follow new host contents, a residue
+    append replays the same capture, a new host buffer re-captures, and
+    ShardedDecoder.step(q_host, out=...) takes the same path."""
+    _, _, _, _, CS = _pk()
+    from paper_2512_24449_b200.attention_sim import GraphedAttention
+    from paper_2512_24449_b200 import sharding as S
+    rng = np.random.default_rng(41)
+    B, H, G, D, T = 2, 2, 4, 128, 64 * 6 + 11
+    st = CS(1, H, D, batch=B)
+    kk, vv = _kv(rng, T + 3, H, D, batch=B)
+    st.compress_batch(0, kk[:, :T], vv[:, :T])
+    ga_d, ga_h = GraphedAttention(st, 0), GraphedAttention(st, 0)
+    qh = torch.empty((B, H * G, D)).pin_memory()
+    oh = torch.empty((B, H * G, D)).pin_memory()
+    for step in range(3):
+        qh.copy_(torch.from_numpy(rng.standard_normal((B, H * G, D)).astype(np.float32)))
+        ref = ga_d(qh.cuda()).cpu()
+        got = ga_h(qh, out=oh)
+        torch.cuda.synchronize()
+        assert got.data_ptr() == oh.data_ptr()
+        assert torch.allclose(oh, ref, rtol=1e-6, atol=1e-6 * float(ref.abs().max()))
+        if step == 1:  # a residue token: same capture
+            st.append_token(0, kk[:, T], vv[:, T])
+    assert ga_h.captures == 1
+    qh2 = qh.clone().pin_memory()
+    o2 = ga_h(qh2).cpu()  # new host buffer, device output: re-capture
+    assert ga_h.captures == 2
+    assert torch.allclose(o2, ga_d(qh2.cuda()).cpu(), rtol=1e-6, atol=1e-6 * float(o2.abs().max()))
+    part = S.plan_partition(B, H, 1, 0)
+    dec = S.ShardedDecoder(part, ga_h, H * G, D)
+    oh2 = torch.empty(B * H * G * D).pin_memory()
+    dec.step(qh, out=oh2)
+    torch.cuda.synchronize()
+    assert torch.allclose(oh2.view(B, H * G, D), ga_d(qh.cuda()).cpu(), rtol=1e-6, atol=1e-6 * float(oh2.abs().max()))
