@@ -1037,7 +1037,8 @@ def test_iterate_blocks_matches_oracle(repack):
             assert (res.layer, res.tokens, res.token_start) == (layer, nres, (T0 + A) // 64 * 64)
 
 
-def test_graphed_attention_zero_copy_host_io():
+@pytest.mark.parametrize("single_pass", [None, True, False])
+def test_graphed_attention_zero_copy_host_io(single_pass):
     """GraphedAttention with pinned host q / out: the graph reads q from host memory
     (pkv_copy_scaled, prescale folded in) and writes the output to host memory; equal to
     the device-q replay (<= 1e-6 relative), replays follow new host contents, a residue
@@ -1052,6 +1053,7 @@ def test_graphed_attention_zero_copy_host_io():
     kk, vv = _kv(rng, T + 3, H, D, batch=B)
     st.compress_batch(0, kk[:, :T], vv[:, :T])
     ga_d, ga_h = GraphedAttention(st, 0), GraphedAttention(st, 0)
+    ga_d.single_pass = ga_h.single_pass = single_pass  # None: the heuristic; True / False: either attention path
     qh = torch.empty((B, H * G, D)).pin_memory()
     oh = torch.empty((B, H * G, D)).pin_memory()
     for step in range(3):
