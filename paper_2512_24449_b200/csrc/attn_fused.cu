@@ -667,23 +667,21 @@ __global__ void __launch_bounds__(128 * kMQ) attn_merge_kernel(pkv_layer_t L, in
       z = fmaf(e, zs, z);
       l = fmaf(e, ls, l);
     };
-    int s = qq;
-    for (; s + 7 * kMQ < ns; s += 8 * kMQ) {  // eight slots' loads in flight (one round for <= 64 slots)
+    // eight slots' loads in flight per round (one round for <= 64 slots): a partial
+    // round loads a valid slot again (index clamped, loads unconditional) and folds
+    // it as empty (M = -inf is a no-op), instead of a tail of dependent single-slot loads
+    for (int s = qq; s < ns; s += 8 * kMQ) {
       float Mv[8], av[8], zv[8], lv[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float* ps = pg + (s + i * kMQ) * st;
+        const float* ps = pg + min(s + i * kMQ, ns - 1) * st;
         Mv[i] = ps[kD + 2];
         av[i] = ps[c];
         zv[i] = ps[kD];
         lv[i] = ps[kD + 1];
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) fold(Mv[i], av[i], zv[i], lv[i]);
-    }
-    for (; s < ns; s += kMQ) {
-      const float* ps = pg + s * st;
-      fold(ps[kD + 2], ps[c], ps[kD], ps[kD + 1]);
+      for (int i = 0; i < 8; ++i) fold(s + i * kMQ < ns ? Mv[i] : -INFINITY, av[i], zv[i], lv[i]);
     }
     ro[qq][c] = o;
     if (c == 0) {
