@@ -60,6 +60,10 @@ def _worker(rank, world, port, B, H, G, D, T, prefer, ret):
         assert tuple(ql.shape) == (p.local_batch, p.local_heads * G, D)
         assert torch.equal(ql, torch.from_numpy(q)[p.b0:p.b1, p.h0 * G:p.h1 * G])
         out = dec.step(ql)
+        # a caller-provided host output buffer receives the same gathered result
+        host = torch.full((B * H * G * D,), float("nan"))
+        assert dec.step(ql, out=host) is host
+        assert torch.equal(host.view(out.shape), out)
         ret[rank] = out.numpy()
     finally:
         dist.destroy_process_group()
