@@ -520,13 +520,14 @@ def run_streaming(args, rank, world, local, backend):
         st2.compress_batch(l, gauss_outlier((B, T0, H, D), n_outlier=4, seed=11 + l),
                            gauss_outlier((B, T0, H, D), n_outlier=1, seed=13 + l))
     loop2 = GraphedDecodeLoop(st2, Hq, headroom=16)
-    loop2.step(kh[0].cuda(), vh[0].cuda(), qh[0].cuda())
+    loop2.step(kh[0].cuda(), vh[0].cuda(), qh[0].cuda(), out=oh)  # captures with the host output buffer
     torch.cuda.synchronize()
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a0.record()
     for i in range(1, E2E):
-        o = loop2.step(kh[i], vh[i], qh[i])  # pinned host -> the graph's input buffers
-        oh.copy_(o, non_blocking=True)
+        # pinned host k/v/q -> the graph's input buffers (copy engine); every layer's output
+        # stored straight to pinned host memory by the attention kernels (zero-copy)
+        loop2.step(kh[i], vh[i], qh[i], out=oh)
     a1.record()
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks([a0.elapsed_time(a1) / (E2E - 1)], world)[0]
@@ -552,7 +553,7 @@ def run_streaming(args, rank, world, local, backend):
                     "h2d_bytes_per_step": Ly * B * (2 * H * D * 2 + Hq * D * 4),
                     "d2h_bytes_per_step": Ly * B * Hq * D * 4,
                     "tokens_per_s": round(world * 1e3 / e2e_ms, 1), "ms_per_step": round(e2e_ms, 5),
-                    "path": "GraphedDecodeLoop.step from pinned host k/v/q, output copied back each step"},
+                    "path": "GraphedDecodeLoop.step(k, v, q, out=host) from pinned host k/v/q; the attention kernels store every layer's output to the pinned host buffer inside the graph"},
             "gpu_launches": timed * (Ly * 3 + 1), "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -360,6 +360,7 @@ class GraphedDecodeLoop:
         self._graph = None
         self._key = None
         self._pool = None
+        self._hout = None  # pinned host output buffer the graph writes, or None (self.out)
         self.captures = 0
 
     def inputs(self):
@@ -371,6 +372,7 @@ class GraphedDecodeLoop:
             ls = self.store[l]
             st.append((ls.arena.data_ptr(), ls.blk_off.data_ptr(), ls.stage.data_ptr(), ls.a_scratch.data_ptr(),
                        ls.max_blocks))
+        st.append(ptr_of(self._hout))
         return tuple(st)
 
     def _prepare(self):
@@ -419,7 +421,8 @@ class GraphedDecodeLoop:
             sp = self.single_pass
             if sp is None:
                 sp = single_pass_preferred(o, self._cap[i])
-            attention_decode_batched(o, l, self._qs[i], scores=self._scores[i], out=self.out[i], nblocks=self._cap[i],
+            dst = self.out[i] if self._hout is None else self._hout[i]  # host: the last kernel stores there
+            attention_decode_batched(o, l, self._qs[i], scores=self._scores[i], out=dst, nblocks=self._cap[i],
                                      single_pass=sp, prescaled=True)
 
     def _capture(self):
@@ -443,12 +446,21 @@ class GraphedDecodeLoop:
         self._key = self._state()
         self.captures += 1
 
-    def step(self, k=None, v=None, q=None, active=None) -> torch.Tensor:
+    def step(self, k=None, v=None, q=None, active=None, out=None) -> torch.Tensor:
         """active (optional, [B] bool / 0-1): the sequences that append a token
         this step (the others only attend); their lengths then diverge on the
-        device (a ragged batch, pkv_append_flush_masked)."""
+        device (a ragged batch, pkv_append_flush_masked).  out (optional, pinned
+        host f32 [layers, B, Hq, D]): the attention kernels store every layer's
+        output straight into it inside the graph (zero-copy; its address is part
+        of the capture, so reuse one buffer); the return value is then `out`."""
         import numpy as np
         o = self.store
+        if out is not None:
+            if out.is_cuda or not out.is_pinned() or out.dtype != torch.float32 or not out.is_contiguous() \
+                    or tuple(out.shape) != tuple(self.out.shape):
+                raise E.ShapeMismatchError(f"out must be a pinned host f32 tensor of shape {tuple(self.out.shape)}")
+        if ptr_of(out) != ptr_of(self._hout):
+            self._hout = out  # a different output target: the capture key changes
         for dst, src in ((self.k, k), (self.v, v), (self.q, q)):
             if src is not None and src.data_ptr() != dst.data_ptr():
                 dst.copy_(src.reshape(dst.shape), non_blocking=True)
@@ -480,7 +492,7 @@ class GraphedDecodeLoop:
             ls.tail_ub += int(done.sum()) * 2 * o.heads * ls.blk_max
             ls.nblk_h, ls.nres_h = int(nblk.max()), int(nres.max())
             ls.ragged = ls.ragged or not (np.all(nblk == nblk[0]) and np.all(nres == nres[0]))
-        return self.out
+        return self.out if self._hout is None else self._hout
 
 def attention_decode(store: CompressedStore, layer: int, head: int, q) -> torch.Tensor:
     """SPEC.md:520-528 (batch 1, one head)."""

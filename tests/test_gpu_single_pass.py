@@ -302,3 +302,36 @@ def test_ragged_prefill_then_decode():
         pos += 1
     for b in range(B):
         assert st[0].stream_bytes(b) == refs[b][0].stream_bytes(0)
+
+
+@pytest.mark.parametrize("single", [True, False])
+def test_decode_loop_host_output(single):
+    """GraphedDecodeLoop.step(..., out=pinned host buffer): the attention kernels store
+    every layer's output straight to host memory inside the graph.  Equal (bit for bit)
+    to a twin loop writing its device buffer, across block completions and re-captures;
+    switching back to device output re-captures."""
+    N, A, CS = _mods()
+    from paper_2512_24449_b200.attention_sim import GraphedDecodeLoop
+    rng = np.random.default_rng(77)
+    B, H, G, Ly, D, T0, steps = 2, 2, 4, 2, 128, 100, 90
+    k = rng.standard_normal((Ly, B, T0 + steps, H, D)).astype(np.float16)
+    v = rng.standard_normal((Ly, B, T0 + steps, H, D)).astype(np.float16)
+    q = rng.standard_normal((steps, Ly, B, H * G, D)).astype(np.float32)
+    a, r = CS(Ly, H, D, batch=B, check=False), CS(Ly, H, D, batch=B, check=False)
+    for l in range(Ly):
+        a.compress_batch(l, k[l, :, :T0], v[l, :, :T0])
+        r.compress_batch(l, k[l, :, :T0], v[l, :, :T0])
+    la, lr = GraphedDecodeLoop(a, H * G, headroom=1), GraphedDecodeLoop(r, H * G, headroom=1)
+    la.single_pass = lr.single_pass = single
+    kd, vd, qd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    host = torch.empty((Ly, B, H * G, D)).pin_memory()
+    for t in range(steps):
+        sl = slice(T0 + t, T0 + t + 1)
+        got = la.step(kd[:, :, sl], vd[:, :, sl], qd[t], out=host)
+        ref = lr.step(kd[:, :, sl], vd[:, :, sl], qd[t])
+        torch.cuda.synchronize()
+        assert got.data_ptr() == host.data_ptr()
+        assert torch.equal(host, ref.cpu()), t
+    caps = la.captures
+    dev = la.step(kd[:, :, T0 + steps - 1:T0 + steps], vd[:, :, T0 + steps - 1:T0 + steps], qd[0])
+    assert dev.is_cuda and la.captures == caps + 1
