@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kWA * 32, MB)
   float* qsm = (float*)(wsm + 3072);           // [G][128] residue chunks: the q copy (K step)
   FeedA F;
   F.init(wsm + kTileA, lane);
+  F.evf = true;  // the partials stay in L2 for the merge
   __syncthreads();
   // decode loop (PDL): the prologue above overlaps the previous kernel (the
   // layer's append-flush); the tables, arena and staging rows it writes are

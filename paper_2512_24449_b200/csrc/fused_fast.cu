@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(kWK * 32, PKV_KMINB) fused_k_fast_kernel(pkv_l
   uint8_t* tile = wsm;
   FeedK F;
   F.init(wsm + kTile, lane);
+  F.evf = ST;  // attention: the score rows stay in L2 for fused V
   __syncthreads();
   const uint32_t tile_s = smem_u32(tile);
   const uint8_t* lutb = (const uint8_t*)lut;
@@ -501,6 +502,7 @@ __global__ void __launch_bounds__(kWV * 32, NT == 2 ? PKV_VMINB2 : PKV_VMINB) fu
   uint8_t* frag = wsm;
   FeedV F;
   F.init(wsm + 2048, lane);
+  F.evf = SM;  // attention: the partials stay in L2 for the finalize
   __syncthreads();
   const uint8_t* lutb = (const uint8_t*)lut;
   const int64_t nwarps = int64_t(gridDim.x) * kWV, wid = int64_t(blockIdx.x) * kWV + warp;
